@@ -1,0 +1,85 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NONE of the method's arithmetic: it draws random action
+tensors with numpy and builds canonical state records (SURVEY §8b layout) from
+ASCII maps for fixtures.  Both the oracle (``oracle/``) and the product
+(``paper_2407_19396_b200``) consume what it produces; neither is imported here.
+
+Canonical per-env record:
+  H*W cells as (type, colour, state) in MiniGrid's encoding, row-major
+  (y outer, x inner); agent x, y, dir; carry (type, colour), (1, 0) = nothing;
+  step_count u16 LE; episode u32 LE; prev_done u8; DynObs: n x (x, y).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# MiniGrid OBJECT_TO_IDX / COLOR_TO_IDX / STATE_TO_IDX values (data format).
+EMPTY, WALL, FLOOR, DOOR, KEY, BALL, BOX, GOAL, LAVA = 1, 2, 3, 4, 5, 6, 7, 8, 9
+RED, GREEN, BLUE, PURPLE, YELLOW, GREY = 0, 1, 2, 3, 4, 5
+OPEN, CLOSED, LOCKED = 0, 1, 2
+
+# ASCII legend for fixture maps.  Door/key/ball colours come from `colors`.
+_LEGEND = {
+    "#": (WALL, GREY, 0),
+    ".": (EMPTY, 0, 0),
+    "A": (EMPTY, 0, 0),  # agent cell (nothing under it)
+    "G": (GOAL, GREEN, 0),
+    "V": (LAVA, RED, 0),
+    "K": (KEY, YELLOW, 0),
+    "B": (BALL, BLUE, 0),
+    "O": (DOOR, YELLOW, OPEN),
+    "D": (DOOR, YELLOW, CLOSED),
+    "L": (DOOR, YELLOW, LOCKED),
+}
+
+
+def random_actions(seed: int, steps: int, n: int, n_actions: int, high: int | None = None) -> np.ndarray:
+    """uint8[steps, n] uniform over [0, high or n_actions) from numpy's PCG64."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, high if high is not None else n_actions, size=(steps, n), dtype=np.uint8)
+
+
+def record_from_map(rows: list[str], agent_dir: int, *, carry=(EMPTY, 0), step_count: int = 0,
+                    episode: int = 0, prev_done: int = 0, colors: dict | None = None,
+                    balls: list[tuple[int, int]] | None = None) -> np.ndarray:
+    """Canonical record for one env from an ASCII map (rows = y, columns = x)."""
+    H, W = len(rows), len(rows[0])
+    colors = colors or {}
+    out = []
+    ax = ay = None
+    for y, row in enumerate(rows):
+        assert len(row) == W
+        for x, ch in enumerate(row):
+            t, c, s = _LEGEND[ch]
+            if ch in colors:
+                c = colors[ch]
+            if ch == "A":
+                ax, ay = x, y
+            out += [t, c, s]
+    assert ax is not None, "map needs an 'A'"
+    out += [ax, ay, agent_dir, carry[0], carry[1]]
+    out += list(int(step_count).to_bytes(2, "little"))
+    out += list(int(episode).to_bytes(4, "little"))
+    out += [prev_done]
+    for bx, by in balls or []:
+        out += [bx, by]
+    return np.array(out, np.uint8)
+
+
+def decode_record(rec: np.ndarray, H: int, W: int, n_obstacles: int = 0) -> dict:
+    """Split a canonical record into named fields (inverse of record_from_map)."""
+    rec = np.asarray(rec, np.uint8)
+    cells = rec[: 3 * H * W].reshape(H, W, 3)
+    p = 3 * H * W
+    d = {
+        "cells": cells,
+        "agent": (int(rec[p]), int(rec[p + 1]), int(rec[p + 2])),
+        "carry": (int(rec[p + 3]), int(rec[p + 4])),
+        "step_count": int(rec[p + 5]) | (int(rec[p + 6]) << 8),
+        "episode": int.from_bytes(bytes(rec[p + 7: p + 11]), "little"),
+        "prev_done": int(rec[p + 11]),
+    }
+    q = p + 12
+    d["balls"] = [(int(rec[q + 2 * i]), int(rec[q + 2 * i + 1])) for i in range(n_obstacles)]
+    return d
