@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the batched MiniGrid step (BASELINE.json metric).
+
+`python bench.py --gpus N --steps K --warmup W` (N > 1 under torchrun, one rank
+per GPU) prints ONE JSON line on rank 0:
+  env-steps/s of DoorKey-8x8 (device-timed, whole box, weak scaling at
+  --envs-per-gpu envs per GPU), the HBM roofline fraction of the step kernel,
+  an end-to-end number through the host-buffer C-ABI call, the CPU oracle
+  timed on this host (cpu_baseline), clocks sampled during the timed region.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on
+rank 0 and prints its line; other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec (device-timed, whole box) DoorKey-8x8 at 1/2/4/8 B200; % HBM roofline"
+UNIT = "env-steps/s"
+
+
+def algorithmic_bytes(spec) -> int:
+    """1 action + H*W grid + 8 + 8 agent record r/w + 147 obs + 4 reward
+    + 2 flags (+ 8 Dynamic-Obstacles ball positions r/w) per env-step."""
+    b = 1 + spec.height * spec.width + 8 + 8 + 147 + 4 + 2
+    if spec.family == 2:
+        b += 8
+    return b
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def committed_traffic(env_id: str):
+    """dram bytes per env-step of the step kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(env_id)
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled in a thread during the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period, self.ok = period_s, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # pragma: no cover - no NVML
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def time_oracle(env_id: str, n_envs: int, steps: int, warmup: int, env_begin: int = 0, n_total=None):
+    """Time the CPU oracle (single thread) on `n_envs` envs: returns env-steps/s."""
+    from oracle import OracleEnv, sample_actions
+    o = OracleEnv(env_id, n_envs, seed=0, env_begin=env_begin, num_envs_total=n_total)
+    o.reset()
+    acts = sample_actions(1, env_begin, n_envs, 0, warmup + steps, o.spec.n_actions)
+    for t in range(warmup):
+        o.step(acts[t])
+    t0 = time.perf_counter()
+    for t in range(warmup, warmup + steps):
+        o.step(acts[t])
+    dt = time.perf_counter() - t0
+    return n_envs * steps / dt, dt
+
+
+def calibrate_oracle(env_id: str) -> float:
+    rate, _ = time_oracle(env_id, 256, 40, 2)
+    return rate
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    model, ncpu = cpu_info()
+    rate = calibrate_oracle(args.env)
+    # bounded sample per step: the whole (warmup + steps) run within ~budget seconds
+    budget = args.ref_budget_s
+    n_ref = int(max(16, min(args.envs_per_gpu, rate * budget / max(1, args.warmup + args.steps))))
+    value, dt = time_oracle(args.env, n_ref, args.steps, args.warmup)
+    sample = (f"{n_ref} envs (global indices 0..{n_ref - 1}) of the {args.env} workload per step, "
+              f"{args.steps} timed steps after {args.warmup} warm-up, single-threaded C++ oracle, {model}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+        "host": {"cpu_model": model, "nproc": ncpu},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {
+        "workload": f"{args.env}, {args.envs_per_gpu} envs per GPU ({args.envs_per_gpu * world} total), "
+                    f"uniform random policy (Philox action stream), auto-reset, symbolic 7x7x3 obs",
+        "env_id": args.env, "envs_per_gpu": args.envs_per_gpu, "global_envs": args.envs_per_gpu * world,
+        "parallelism": f"env-sharded x{world} (NCCL all-reduce of int64[8] episode stats only)",
+        "l2": "inputs larger than L2: per step per GPU ~230 MB (state 76 MB read+write, obs 154 MB) vs 126 MB L2",
+        "graph": "CUDA graph of the timed steps (one step kernel launch per step)",
+    }
+
+
+def run_navix(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2407_19396_b200 import NavixEnv, shard_range
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    n_total = args.envs_per_gpu * world
+    begin, end = shard_range(n_total, rank, world)
+    n = end - begin
+    env = NavixEnv(args.env, n, seed=0, env_begin=begin, num_envs_total=n_total, device=dev)
+    spec = env.spec
+    B = algorithmic_bytes(spec)
+    env.reset()
+    ring = min(args.steps, args.action_ring)
+    acts = env.sample_actions(1, 0, ring)  # random policy, inputs resident in HBM
+    s = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for t in range(args.warmup):
+        env.step(acts[t % ring])
+    barrier()
+
+    # capture the timed steps as CUDA graphs (chunks of `ring` steps)
+    graphs = []
+    remaining = args.steps
+    if not args.no_graph:
+        torch.cuda.synchronize(dev)
+        while remaining > 0:
+            k = min(ring, remaining)
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                for t in range(k):
+                    env.step(acts[t])
+            graphs.append(gph)
+            remaining -= k
+        # graph capture does not execute; warm the graphs once (untimed)
+        for gph in graphs:
+            gph.replay()
+    barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(s)
+        if graphs:
+            for gph in graphs:
+                gph.replay()
+        else:
+            for t in range(args.steps):
+                env.step(acts[t % ring])
+        ev1.record(s)
+        torch.cuda.synchronize(dev)
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    t_max = t_local
+    if dist is not None:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = n_total * args.steps / t_max
+
+    # episode statistics: the one collective of the path (NCCL all-reduce of int64[8])
+    st = env.stats().clone()
+    if dist is not None:
+        dist.all_reduce(st)
+    st = st.cpu().numpy()
+
+    # end to end through the host-buffer C-ABI call (H2D actions, D2H outputs)
+    h_act = torch.from_numpy(np.ascontiguousarray(acts[: args.e2e_steps].cpu().numpy())).pin_memory()
+    h_obs = torch.empty((n, 7, 7, 3), dtype=torch.uint8).pin_memory()
+    h_rew = torch.empty(n, dtype=torch.float32).pin_memory()
+    h_te = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_tr = torch.empty(n, dtype=torch.uint8).pin_memory()
+    env.step_host(h_act[0], h_obs, h_rew, h_te, h_tr)  # allocates staging (untimed)
+    barrier()
+    t0 = time.perf_counter()
+    for t in range(args.e2e_steps):
+        env.step_host(h_act[t], h_obs, h_rew, h_te, h_tr)
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = n_total * args.e2e_steps / t_e2e
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peaks()
+    per_launch_s = t_local / args.steps
+    achieved = B * n / per_launch_s / 1e9
+    traffic = committed_traffic(args.env)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None if traffic is None else traffic * n,
+            "algorithmic_bytes_per_env_step": B, "envs_per_launch": n, "kernel": "navix_kernel<DoorKey,8,8,STEP>",
+            "peak_source": peak_src}
+    model, ncpu = cpu_info()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        n_cpu = args.cpu_envs
+        v, dt = time_oracle(args.env, n_cpu, args.cpu_steps, 2)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{n_cpu} envs x {args.cpu_steps} steps of {args.env} (global indices 0..{n_cpu - 1}, "
+                         f"same seeds and Philox action stream), single-threaded C++ oracle, {dt:.1f} s, {model}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(args, world),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_total,
+                "d2h_bytes_per_step": n_total * (147 + 4 + 1 + 1), "steps": args.e2e_steps,
+                "api": "navix_step_host (pinned host buffers)"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "episode_stats": {k: int(v) for k, v in zip(
+            ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_collision", "n_truncated",
+             "gen_failures"), st)},
+        "host": {"cpu_model": model, "nproc": ncpu},
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="navix", choices=["navix", "reference"])
+    ap.add_argument("--env", default="DoorKey-8x8-v0")
+    ap.add_argument("--envs-per-gpu", type=int, default=1 << 20)
+    ap.add_argument("--action-ring", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-envs", type=int, default=4096)
+    ap.add_argument("--cpu-steps", type=int, default=1000)
+    ap.add_argument("--ref-budget-s", type=float, default=60.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_navix(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -83,3 +83,59 @@ def decode_record(rec: np.ndarray, H: int, W: int, n_obstacles: int = 0) -> dict
     q = p + 12
     d["balls"] = [(int(rec[q + 2 * i]), int(rec[q + 2 * i + 1])) for i in range(n_obstacles)]
     return d
+
+
+def random_records(seed: int, n: int, H: int, W: int, max_steps: int, n_obstacles: int = 0,
+                   p_prev_done: float = 0.0) -> np.ndarray:
+    """n canonical records of random but legal states: wall border, random
+    interior objects (walls, doors in all three states, keys, balls, boxes,
+    goals, lava, floor), the agent on a walkable interior cell, a random
+    carried object, random step count.  With n_obstacles > 0 (DynObs) exactly
+    that many blue balls are listed (extra balls may still appear as static
+    objects)."""
+    rng = np.random.default_rng(seed)
+    kinds = np.array([EMPTY, WALL, DOOR, KEY, BALL, BOX, GOAL, LAVA, FLOOR])
+    probs = np.array([0.42, 0.16, 0.12, 0.07, 0.06, 0.04, 0.05, 0.05, 0.03])
+    per = 3 * H * W + 12 + 2 * n_obstacles
+    out = np.zeros((n, per), np.uint8)
+    for e in range(n):
+        cells = np.zeros((H, W, 3), np.uint8)
+        cells[:, :, 0] = WALL
+        cells[:, :, 1] = GREY
+        for y in range(1, H - 1):
+            for x in range(1, W - 1):
+                k = rng.choice(kinds, p=probs)
+                c = int(rng.integers(0, 6))
+                if k == EMPTY:
+                    cells[y, x] = (EMPTY, 0, 0)
+                elif k == DOOR:
+                    cells[y, x] = (DOOR, c, int(rng.integers(0, 3)))
+                else:
+                    cells[y, x] = (k, c, 0)
+        walk = [(x, y) for y in range(1, H - 1) for x in range(1, W - 1)
+                if cells[y, x, 0] in (EMPTY, FLOOR, GOAL, LAVA) or (cells[y, x, 0] == DOOR and cells[y, x, 2] == OPEN)]
+        if not walk:
+            x, y = 1, 1
+            cells[y, x] = (EMPTY, 0, 0)
+            walk = [(1, 1)]
+        ax, ay = walk[int(rng.integers(len(walk)))]
+        balls = []
+        if n_obstacles:
+            free = [(x, y) for y in range(1, H - 1) for x in range(1, W - 1) if (x, y) != (ax, ay)]
+            pick = rng.permutation(len(free))[:n_obstacles]
+            for i in pick:
+                bx, by = free[i]
+                cells[by, bx] = (BALL, BLUE, 0)
+                balls.append((bx, by))
+        ck = int(rng.integers(0, 4))
+        carry = (EMPTY, 0) if ck == 0 else ((KEY, BALL, BOX)[ck - 1], int(rng.integers(0, 6)))
+        rec = list(cells.reshape(-1))
+        sc = int(rng.integers(0, max_steps))
+        rec += [ax, ay, int(rng.integers(0, 4)), carry[0], carry[1]]
+        rec += list(sc.to_bytes(2, "little"))
+        rec += list(int(rng.integers(0, 1000)).to_bytes(4, "little"))
+        rec += [int(rng.random() < p_prev_done)]
+        for bx, by in balls:
+            rec += [bx, by]
+        out[e] = rec
+    return out

@@ -1,0 +1,110 @@
+// layout.h — internal data layout of libnavix (host + device).
+//
+// HBM state of one handle (one shard), a single allocation:
+//   grid    u64 [n_tiles][H][TILE]   row y of env (tile, lane): 8 cell bytes,
+//                                     byte x = cell (x, y); bytes x >= W are 0
+//   agent   u64 [n_pad]               agent record (below)
+//   episode u32 [n_pad]               episode counter (counter word c1, R#20)
+//   balls   u32 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b
+//   stats   u64 [NSLOT][8]            striped int64 episode statistics
+// n_pad = num_envs rounded up to TILE.  The struct-of-arrays "row plane"
+// layout makes every warp load of a grid row one contiguous 256-byte segment
+// and lets the kernel fetch a whole world row with one 64-bit load.
+//
+// Cell byte: bit 7 = opaque (wall, closed door, locked door: see_behind is
+// False), bits 4-6 = MiniGrid colour, bits 0-3 = kind:
+//   1 empty, 2 wall, 3 floor, 4 open door, 5 key, 6 ball, 7 box, 8 goal,
+//   9 lava, 11 closed door, 12 locked door.   0 = outside the grid.
+// obs type = kind >= 11 ? 4 : kind; obs state = kind >= 11 ? kind - 10 : 0;
+// obs colour = bits 4-6.  Dynamic-Obstacles balls are NOT stored in the HBM
+// grid (it holds the static layout); they are overlaid from `balls` in SMEM.
+//
+// Agent record (u64, little endian bytes): 0 x, 1 y, 2 dir, 3 carry (cell
+// byte of the carried object, 0x01 = nothing), 4-5 step_count, 6 flags
+// (bit 0 prev_done), 7 unused.
+#pragma once
+#include <cstdint>
+
+namespace navix {
+
+constexpr int TILE = 128;   // envs per CTA (one thread per env)
+constexpr int NSLOT = 512;  // stats stripes (atomics spread over 512 x 64 B)
+constexpr int OBS_BYTES = 147;
+
+enum Kind : uint8_t {
+  K_OOB = 0, K_EMPTY = 1, K_WALL = 2, K_FLOOR = 3, K_DOOR_OPEN = 4, K_KEY = 5, K_BALL = 6,
+  K_BOX = 7, K_GOAL = 8, K_LAVA = 9, K_DOOR_CLOSED = 11, K_DOOR_LOCKED = 12
+};
+constexpr uint8_t OPAQUE_BIT = 0x80;
+
+__host__ __device__ constexpr uint8_t make_cell(uint8_t kind, uint8_t colour) {
+  return (uint8_t)(((kind == K_WALL || kind == K_DOOR_CLOSED || kind == K_DOOR_LOCKED) ? OPAQUE_BIT : 0) |
+                   ((colour & 7) << 4) | kind);
+}
+// MiniGrid colours
+constexpr uint8_t COL_RED = 0, COL_GREEN = 1, COL_BLUE = 2, COL_PURPLE = 3, COL_YELLOW = 4, COL_GREY = 5;
+constexpr uint8_t CELL_EMPTY = make_cell(K_EMPTY, 0);
+constexpr uint8_t CELL_WALL = make_cell(K_WALL, COL_GREY);
+constexpr uint8_t CELL_GOAL = make_cell(K_GOAL, COL_GREEN);
+constexpr uint8_t CELL_LAVA = make_cell(K_LAVA, COL_RED);
+
+enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4 };
+
+struct EnvConfig {
+  int family;
+  int height, width;
+  int max_steps;
+  int n_actions;
+  int n_obstacles;
+  int room_size, num_rows;  // KeyCorridor
+};
+
+// Byte offsets of the arrays inside one state allocation.
+struct StateLayout {
+  int64_t n_pad, n_tiles;
+  size_t grid_off, agent_off, episode_off, balls_off, stats_off, total;
+};
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
+  StateLayout L{};
+  L.n_tiles = (n + TILE - 1) / TILE;
+  L.n_pad = L.n_tiles * TILE;
+  size_t off = 0;
+  L.grid_off = off;
+  off = align_up(off + (size_t)L.n_pad * c.height * 8, 256);
+  L.agent_off = off;
+  off = align_up(off + (size_t)L.n_pad * 8, 256);
+  L.episode_off = off;
+  off = align_up(off + (size_t)L.n_pad * 4, 256);
+  L.balls_off = off;
+  off = align_up(off + (c.family == FAM_DYNOBS ? (size_t)L.n_pad * 4 : 0), 256);
+  L.stats_off = off;
+  off = align_up(off + (size_t)NSLOT * 8 * 8, 256);
+  L.total = off;
+  return L;
+}
+
+// Kernel arguments (by value).
+struct KernelArgs {
+  uint64_t* grid;
+  uint64_t* agent;
+  uint32_t* episode;
+  uint32_t* balls;
+  unsigned long long* stats;
+  const uint8_t* actions;
+  uint8_t* obs;
+  float* reward;
+  uint8_t* terminated;
+  uint8_t* truncated;
+  int64_t n;            // local envs
+  uint32_t env_begin;   // global index of local env 0 (Philox counter word c0)
+  uint32_t key_lo, key_hi;
+  int reward_mode;
+  int bulk_obs;         // 1: obs base is 16-B aligned -> cp.async.bulk store of full tiles
+};
+
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2 };
+
+}  // namespace navix

@@ -1,0 +1,236 @@
+// levelgen.cuh — device level generators: the starting distribution P0 of
+// reset(key) for the Table 9 families, with
+// MiniGrid's layouts.  One thread generates one env's level into its
+// SMEM row lines.  Draws follow DESIGN.md R#20-R#25: Philox stream
+// (global env, episode, 0, block); rejection loops replaced by one uniform
+// draw over the admissible set in row-major order; connect_all keeps its loop.
+#pragma once
+#include "layout.h"
+#include "philox.cuh"
+
+namespace navix {
+
+// Compile-time configuration of one kernel instantiation.
+template <int FAM, int H, int W>
+struct Cfg {
+  static constexpr int RS = 3;                       // KeyCorridor room size (W <= 8 -> 3)
+  static constexpr int NR = (H - 1) / (RS - 1);      // KeyCorridor rows
+  static constexpr int T = FAM == FAM_DOORKEY ? 10 * W * W
+                         : FAM == FAM_KEYCORRIDOR ? 30 * RS * RS
+                         : 4 * W * H;                // R#16
+  static constexpr int NA = FAM == FAM_DYNOBS ? 3 : 7;
+  static constexpr int NOBST = FAM != FAM_DYNOBS ? 0 : (W == 5 ? 2 : W == 6 ? 3 : 4);  // R#6
+};
+
+// Static layout row y as 8 cell bytes (bytes >= W are 0 = outside the grid).
+template <int FAM, int H, int W>
+__host__ __device__ constexpr uint64_t template_row(int y) {
+  uint64_t r = 0;
+  for (int x = 0; x < W; ++x) {
+    bool wall;
+    if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
+    else wall = x == 0 || y == 0 || x == W - 1 || y == H - 1;
+    uint8_t c = wall ? CELL_WALL : CELL_EMPTY;
+    if (FAM != FAM_KEYCORRIDOR && x == W - 2 && y == H - 2) c = CELL_GOAL;  // goal (W-2, H-2)
+    r |= (uint64_t)c << (8 * x);
+  }
+  return r;
+}
+
+// Per-thread view of its env's SMEM row lines: rows[y * TILE] is row y.
+struct RowView {
+  uint64_t* rows;  // &s_rows[0][tid]
+  __device__ __forceinline__ uint8_t* at(int x, int y) const {
+    return reinterpret_cast<uint8_t*>(rows + y * TILE) + x;
+  }
+  __device__ __forceinline__ uint8_t get(int x, int y) const { return *at(x, y); }
+  __device__ __forceinline__ void set(int x, int y, uint8_t v) const { *at(x, y) = v; }
+};
+
+// k-th (0-based) set bit of a 64-bit mask, by binary search on popcounts.
+__device__ __forceinline__ int select64(uint64_t m, uint32_t k) {
+  int pos = 0;
+  uint32_t w = (uint32_t)m;
+  uint32_t c = __popc(w);
+  if (k >= c) { k -= c; w = (uint32_t)(m >> 32); pos = 32; }
+  c = __popc(w & 0xFFFFu);
+  if (k >= c) { k -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xFFu);
+  if (k >= c) { k -= c; w >>= 8; pos += 8; }
+  c = __popc(w & 0xFu);
+  if (k >= c) { k -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);
+  if (k >= c) { k -= c; w >>= 2; pos += 2; }
+  c = w & 1u;
+  if (k >= c) pos += 1;
+  return pos;
+}
+
+struct GenOut {
+  int ax, ay, dir;
+  uint32_t balls;
+  uint32_t fail;
+};
+
+template <int FAM, int H, int W>
+__device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t episode, uint32_t klo,
+                                              uint32_t khi) {
+  using C = Cfg<FAM, H, W>;
+  GenOut o{1, 1, 0, 0u, 0u};
+#pragma unroll
+  for (int y = 0; y < H; ++y) g.rows[y * TILE] = template_row<FAM, H, W>(y);
+  DrawStream ds(genv, episode, 0u, klo, khi);
+
+  if constexpr (FAM == FAM_DOORKEY) {
+    // [MG] DoorKeyEnv._gen_grid: split, agent pos, agent dir, door row, key pos
+    const int split = 2 + (int)ds.next_bounded(W - 4);
+    for (int y = 0; y < H; ++y) g.set(split, y, CELL_WALL);
+    const uint32_t wid = (uint32_t)(split - 1);
+    const uint32_t cnt = wid * (H - 2);          // interior cells left of the wall, all empty
+    const uint32_t ka = ds.next_bounded(cnt);
+    o.ax = 1 + (int)(ka % wid);
+    o.ay = 1 + (int)(ka / wid);
+    o.dir = (int)ds.next_bounded(4);
+    const int door_y = 1 + (int)ds.next_bounded(W - 3);   // R#24
+    g.set(split, door_y, make_cell(K_DOOR_LOCKED, COL_YELLOW));
+    uint32_t kk = ds.next_bounded(cnt - 1);
+    if (kk >= ka) ++kk;                            // skip the agent cell
+    g.set(1 + (int)(kk % wid), 1 + (int)(kk / wid), make_cell(K_KEY, COL_YELLOW));
+  } else if constexpr (FAM == FAM_LAVAGAP) {
+    // [MG] LavaGapEnv._gen_grid
+    const int gx = 2 + (int)ds.next_bounded(W - 4);
+    const int gy = 1 + (int)ds.next_bounded(H - 2);
+    for (int y = 1; y <= H - 2; ++y)
+      if (y != gy) g.set(gx, y, CELL_LAVA);
+  } else if constexpr (FAM == FAM_DYNOBS) {
+    // [MG] DynamicObstaclesEnv._gen_grid: balls uniform over empty cells, not the agent
+    uint64_t freem = 0;
+#pragma unroll
+    for (int y = 1; y <= H - 2; ++y)
+#pragma unroll
+      for (int x = 1; x <= W - 2; ++x) freem |= 1ull << (y * 8 + x);
+    freem &= ~(1ull << ((H - 2) * 8 + (W - 2)));  // goal
+    freem &= ~(1ull << (1 * 8 + 1));              // agent (1, 1)
+#pragma unroll
+    for (int b = 0; b < C::NOBST; ++b) {
+      const uint32_t u = ds.next();
+      const uint32_t cnt = __popcll(freem);
+      if (cnt == 0) { o.fail += 1; continue; }
+      const int pos = select64(freem, bounded(u, cnt));
+      freem &= ~(1ull << pos);
+      const int x = pos & 7, y = pos >> 3;
+      g.set(x, y, make_cell(K_BALL, COL_BLUE));
+      o.balls |= (uint32_t)((x << 4) | y) << (8 * b);
+    }
+  } else if constexpr (FAM == FAM_KEYCORRIDOR) {
+    // [MG] RoomGrid._gen_grid + KeyCorridorEnv._gen_grid + connect_all
+    constexpr int S = C::RS, NR = C::NR, NC = 3, NROOM = NR * NC;
+    uint8_t dpy[NROOM], dpx[NROOM];  // door_pos[0].y and door_pos[1].x per room
+    for (int j = 0; j < NR; ++j)
+      for (int i = 0; i < NC; ++i) {
+        const int r = j * NC + i;
+        if (i < NC - 1) dpy[r] = (uint8_t)(j * (S - 1) + 1 + ds.next_bounded(S - 2));
+        if (j < NR - 1) dpx[r] = (uint8_t)(i * (S - 1) + 1 + ds.next_bounded(S - 2));
+      }
+    const int adx = (NC / 2) * (S - 1) + S / 2, ady = (NR / 2) * (S - 1) + S / 2;  // default agent
+    uint32_t adj[NROOM];
+#pragma unroll
+    for (int r = 0; r < NROOM; ++r) adj[r] = 0;
+    // hallway: remove_wall(1, j, up) for j >= 1
+    for (int j = 1; j < NR; ++j) {
+      for (int t = 1; t < S - 1; ++t) g.set((S - 1) + t, j * (S - 1), CELL_EMPTY);
+      adj[j * NC + 1] |= 1u << ((j - 1) * NC + 1);
+      adj[(j - 1) * NC + 1] |= 1u << (j * NC + 1);
+    }
+    const int room_idx = (int)ds.next_bounded(NR);
+    const uint8_t door_col = (uint8_t)ds.next_bounded(6);           // R#23
+    const int locked_room = room_idx * NC + 2;
+    g.set(2 * (S - 1), dpy[room_idx * NC + 1], make_cell(K_DOOR_LOCKED, door_col));
+    adj[locked_room] |= 1u << (locked_room - 1);
+    adj[locked_room - 1] |= 1u << locked_room;
+    // object placement inside room (ri, rj): empty, not the default agent
+    // cell, Manhattan distance >= 2 from it (reject_next_to, R#25)
+    auto place_in_room = [&](int ri, int rj, uint8_t cell) {
+      const uint32_t u = ds.next();
+      uint32_t m = 0;
+      int n = 0;
+      for (int yy = 0; yy < S; ++yy)
+        for (int xx = 0; xx < S; ++xx) {
+          const int x = ri * (S - 1) + xx, y = rj * (S - 1) + yy;
+          const int d = abs(x - adx) + abs(y - ady);
+          const bool ok = x < W && y < H && g.get(x, y) == CELL_EMPTY && d >= 2;
+          m |= (ok ? 1u : 0u) << (yy * S + xx);
+          n += ok;
+        }
+      if (n == 0) { o.fail += 1; return; }
+      int p = select64(m, bounded(u, (uint32_t)n));
+      g.set(ri * (S - 1) + p % S, rj * (S - 1) + p / S, cell);
+    };
+    const uint8_t ball_col = (uint8_t)ds.next_bounded(6);
+    place_in_room(2, room_idx, make_cell(K_BALL, ball_col));
+    const int kr = (int)ds.next_bounded(NR);
+    place_in_room(0, kr, make_cell(K_KEY, door_col));
+    // place_agent(1, NR/2): (pos, dir) uniform over pairs whose front is empty or a wall
+    {
+      const uint32_t u = ds.next();
+      uint64_t m = 0;
+      int n = 0;
+      const int rx = S - 1, ry = (NR / 2) * (S - 1);
+      for (int yy = 0; yy < S; ++yy)
+        for (int xx = 0; xx < S; ++xx) {
+          const int x = rx + xx, y = ry + yy;
+          if (g.get(x, y) != CELL_EMPTY) continue;
+          for (int d = 0; d < 4; ++d) {
+            const int fx = x + (d == 0) - (d == 2), fy = y + (d == 1) - (d == 3);
+            const uint8_t f = g.get(fx, fy);
+            const bool ok = f == CELL_EMPTY || (f & 15) == K_WALL;
+            m |= (ok ? 1ull : 0ull) << ((yy * S + xx) * 4 + d);
+            n += ok;
+          }
+        }
+      if (n == 0) {
+        o.fail += 1;
+      } else {
+        const int p = select64(m, bounded(u, (uint32_t)n));
+        o.dir = p & 3;
+        o.ax = rx + (p >> 2) % S;
+        o.ay = ry + (p >> 2) / S;
+      }
+    }
+    // connect_all(max_itrs = 5000)
+    const uint32_t all = (1u << NROOM) - 1;
+    const int start = (o.ay / (S - 1)) * NC + o.ax / (S - 1);
+    for (int it = 0;; ++it) {
+      if (it > 5000) { o.fail += 1; break; }
+      uint32_t reach = 1u << start, prev = 0;
+      while (reach != prev) {
+        prev = reach;
+#pragma unroll
+        for (int r = 0; r < NROOM; ++r)
+          if ((reach >> r) & 1u) reach |= adj[r];
+      }
+      if (reach == all) break;
+      const int i = (int)ds.next_bounded(NC);
+      const int j = (int)ds.next_bounded(NR);
+      const int k = (int)ds.next_bounded(4);
+      const int r = j * NC + i;
+      const bool has = k == 0 ? i < NC - 1 : k == 1 ? j < NR - 1 : k == 2 ? i > 0 : j > 0;
+      if (!has) continue;
+      const int nb = k == 0 ? r + 1 : k == 1 ? r + NC : k == 2 ? r - 1 : r - NC;
+      if ((adj[r] >> nb) & 1u) continue;
+      if (r == locked_room || nb == locked_room) continue;
+      const uint8_t col = (uint8_t)ds.next_bounded(6);
+      int x, y;
+      if (k == 0) { x = i * (S - 1) + S - 1; y = dpy[r]; }
+      else if (k == 1) { x = dpx[r]; y = j * (S - 1) + S - 1; }
+      else if (k == 2) { x = (i - 1) * (S - 1) + S - 1; y = dpy[r - 1]; }
+      else { x = dpx[r - NC]; y = (j - 1) * (S - 1) + S - 1; }
+      g.set(x, y, make_cell(K_DOOR_CLOSED, col));
+      adj[r] |= 1u << nb;
+      adj[nb] |= 1u << r;
+    }
+  }
+  return o;
+}
+
+}  // namespace navix

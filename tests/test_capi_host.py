@@ -1,0 +1,78 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports
+every symbol include/navix.h declares, parses Table 9 ids, sizes state, and
+rejects bad arguments with a status and a message."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_are_exported():
+    from paper_2407_19396_b200 import EXPORTED_SYMBOLS, load_library
+    hdr = open(os.path.join(ROOT, "include", "navix.h")).read()
+    declared = set(re.findall(r"NAVIX_API\s+[\w\s\*]+?\b(navix_\w+)\s*\(", hdr))
+    assert declared == set(EXPORTED_SYMBOLS)
+    lib = load_library()
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+@pytest.mark.parametrize("env_id,h,w,T,na,fam", [
+    ("Navix-Empty-5x5-v0", 5, 5, 100, 7, 0),
+    ("MiniGrid-Empty-8x8-v0", 8, 8, 256, 7, 0),
+    ("DoorKey-8x8", 8, 8, 640, 7, 1),
+    ("Navix-Dynamic-Obstacles-8x8-v0", 8, 8, 256, 3, 2),
+    ("Navix-KeyCorridorS3R3-v0", 7, 7, 270, 7, 3),
+    ("KeyCorridorS3R1", 3, 7, 270, 7, 3),
+    ("Navix-LavaGapS7-v0", 7, 7, 196, 7, 4),
+])
+def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
+    from oracle import spec_of as oracle_spec
+    from paper_2407_19396_b200 import spec_of
+    s = spec_of(env_id)
+    assert (s.height, s.width, s.max_steps, s.n_actions, s.family, s.obs_bytes, s.view) == (h, w, T, na, fam, 147, 7)
+    o = oracle_spec(env_id)  # the two independent parsers agree
+    assert (o.height, o.width, o.max_steps, o.n_actions, o.export_bytes) == (h, w, T, na, s.export_bytes)
+
+
+def test_unknown_and_unsupported_ids():
+    from paper_2407_19396_b200 import NavixError, load_library, spec_of
+    with pytest.raises(NavixError) as e:
+        spec_of("Navix-NoSuchEnv-v0")
+    assert e.value.status == 1 and "unknown env id" in str(e.value)
+    s = spec_of("Navix-DoorKey-16x16-v0")  # Table 9 id without a kernel yet: spec still known
+    assert (s.height, s.width, s.max_steps) == (16, 16, 2560)
+    lib = load_library()
+    h = ctypes.c_void_p()
+    assert lib.navix_create_shard(b"DoorKey-16x16", 8, 0, 8, 0, 0, None, 0, ctypes.byref(h)) == 5
+    assert b"no kernel" in lib.navix_last_error()
+
+
+def test_argument_validation_before_any_cuda_call():
+    from paper_2407_19396_b200 import load_library, state_bytes
+    lib = load_library()
+    h = ctypes.c_void_p()
+    assert lib.navix_create_shard(b"DoorKey-8x8-v0", 10, 5, 10, 0, 0, None, 0, ctypes.byref(h)) == 2
+    assert b"outside" in lib.navix_last_error()
+    assert lib.navix_create_shard(b"DoorKey-8x8-v0", 10, 0, 0, 0, 0, None, 0, ctypes.byref(h)) == 2
+    assert lib.navix_create_shard(b"DoorKey-8x8-v0", 10, 0, 10, 0, 0, None, 7, ctypes.byref(h)) == 2
+    assert lib.navix_step(None, None, None, None, None, None, None) == 2
+    assert lib.navix_reset(None, None, None) == 2
+    assert state_bytes("DoorKey-8x8-v0", 0) == 0
+    assert state_bytes("DoorKey-8x8-v0", 1 << 20) >= (1 << 20) * (64 + 8 + 4)
+    assert state_bytes("Foo", 10) == 0
+
+
+def test_shard_ranges_partition():
+    from paper_2407_19396_b200 import shard_range
+    for n in (1, 7, 1000, 1 << 23):
+        for G in (1, 2, 3, 4, 8):
+            if G > n:
+                continue
+            rs = [shard_range(n, r, G) for r in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(e - b for b, e in rs) - min(e - b for b, e in rs) <= 1

@@ -1,0 +1,181 @@
+"""GPU <-> oracle parity through the C ABI (libnavix.so), bit-exact.
+
+Every output of every step (observation bytes, reward bits, terminated,
+truncated) and the canonical state export are compared with the CPU oracle
+on identical seeded inputs (inputgen: numpy PCG64 actions, fed to both
+sides).  Full-batch comparison for the small configs of BASELINE.json; for
+the large configs the GPU runs the full batch in the bench's launch
+configuration and the oracle recomputes contiguous blocks of envs spread over
+the batch (head, middle, ragged tail), which it can afford one by one.
+"""
+import numpy as np
+import pytest
+import torch
+
+from inputgen import random_actions
+from oracle import OracleEnv, sample_actions as oracle_sample_actions
+
+pytestmark = pytest.mark.gpu
+
+
+def navix():
+    from paper_2407_19396_b200 import NavixEnv
+    return NavixEnv
+
+
+def _blocks(n, block):
+    if n <= 4 * block:
+        return [(0, n)]
+    mid = (n // 2) // 128 * 128 + 37
+    return [(0, block), (mid, mid + block), (n - block, n)]
+
+
+def run_parity(env_id, n, steps, seed=0, action_seed=1, block=128, reward_mode=0, export_every=50):
+    NavixEnv = navix()
+    g = NavixEnv(env_id, n, seed=seed, reward_mode=reward_mode)
+    blocks = _blocks(n, block)
+    oracles = [OracleEnv(env_id, e - b, seed=seed, env_begin=b, num_envs_total=n, reward_mode=reward_mode)
+               for b, e in blocks]
+    idx = torch.cat([torch.arange(b, e) for b, e in blocks]).cuda()
+    obs = g.reset()
+    o_obs = np.concatenate([o.reset() for o in oracles])
+    np.testing.assert_array_equal(obs[idx].cpu().numpy(), o_obs)
+    acts = random_actions(action_seed, steps, n, g.spec.n_actions, high=8)  # 8: includes out-of-range 7
+    acts_dev = torch.from_numpy(acts).cuda()
+    for t in range(steps):
+        obs, rew, te, tr = g.step(acts_dev[t])
+        outs = [o.step(acts[t, b:e]) for o, (b, e) in zip(oracles, blocks)]
+        o_obs = np.concatenate([x[0] for x in outs])
+        o_rew = np.concatenate([x[1] for x in outs])
+        o_te = np.concatenate([x[2] for x in outs])
+        o_tr = np.concatenate([x[3] for x in outs])
+        got_obs = obs[idx].cpu().numpy()
+        if not np.array_equal(got_obs, o_obs):
+            bad = np.argwhere((got_obs != o_obs).reshape(len(o_obs), -1).any(1))[:, 0]
+            raise AssertionError(f"{env_id} step {t}: obs differ for {len(bad)} envs, first local {bad[:5]}")
+        np.testing.assert_array_equal(rew[idx].cpu().numpy().view(np.uint32), o_rew.view(np.uint32),
+                                      err_msg=f"reward bits step {t}")
+        np.testing.assert_array_equal(te[idx].cpu().numpy(), o_te, err_msg=f"terminated step {t}")
+        np.testing.assert_array_equal(tr[idx].cpu().numpy(), o_tr, err_msg=f"truncated step {t}")
+        if (t + 1) % export_every == 0 or t == steps - 1:
+            rec = g.export_state()
+            o_rec = np.concatenate([o.export() for o in oracles])
+            np.testing.assert_array_equal(rec[idx.cpu().numpy()], o_rec, err_msg=f"state step {t}")
+    if len(blocks) == 1 and blocks[0] == (0, n):
+        np.testing.assert_array_equal(g.stats().cpu().numpy(), oracles[0].stats())
+    return g
+
+
+def test_parity_cfg1_empty5x5_16_envs_1000_steps():
+    run_parity("Empty-5x5-v0", 16, 1000, export_every=1)
+
+
+@pytest.mark.parametrize("env_id", ["Empty-8x8-v0", "DoorKey-8x8-v0"])
+def test_parity_cfg2_2048_envs_1000_steps(env_id):
+    run_parity(env_id, 2048, 1000, block=2048)
+
+
+def test_parity_cfg3_dynobs_65536():
+    run_parity("Dynamic-Obstacles-8x8-v0", 65536, 1000, block=128)
+
+
+@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "LavaGapS7-v0"])
+def test_parity_cfg4_262144(env_id):
+    run_parity(env_id, 262144, 600, block=128)
+
+
+def test_parity_cfg5_doorkey_1M_sampled():
+    run_parity("DoorKey-8x8-v0", 1 << 20, 300, block=96, export_every=100)
+
+
+@pytest.mark.parametrize("env_id", ["Empty-6x6-v0", "DoorKey-5x5-v0", "DoorKey-6x6-v0",
+                                    "Dynamic-Obstacles-5x5-v0", "Dynamic-Obstacles-6x6-v0",
+                                    "LavaGapS5-v0", "LavaGapS6-v0", "KeyCorridorS3R1-v0",
+                                    "KeyCorridorS3R2-v0"])
+def test_parity_other_sizes_ragged(env_id):
+    # 333 envs: two full tiles and a ragged tail of 77 (plain-store path)
+    run_parity(env_id, 333, 400, block=333, seed=5)
+
+
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "LavaGapS7-v0", "Dynamic-Obstacles-8x8-v0"])
+def test_parity_reward_mode_navix(env_id):
+    run_parity(env_id, 512, 300, block=512, reward_mode=1, seed=9)
+
+
+@pytest.mark.parametrize("n", [1, 7, 128, 129])
+def test_parity_tiny_batches(n):
+    run_parity("DoorKey-8x8-v0", n, 200, block=n, seed=2)
+
+
+def test_sample_actions_matches_oracle():
+    NavixEnv = navix()
+    for env_id in ("DoorKey-8x8-v0", "Dynamic-Obstacles-8x8-v0"):
+        g = NavixEnv(env_id, 1000, env_begin=3000, num_envs_total=10000)
+        a = g.sample_actions(12345, 77, 20).cpu().numpy()
+        b = oracle_sample_actions(12345, 3000, 1000, 77, 20, g.spec.n_actions)
+        np.testing.assert_array_equal(a, b)
+
+
+def test_shard_invariance_and_determinism():
+    NavixEnv = navix()
+    n, steps, G = 1000, 300, 4
+    env_id = "KeyCorridorS3R3-v0"
+    full = NavixEnv(env_id, n, seed=11)
+    full.reset()
+    acts = torch.from_numpy(random_actions(3, steps, n, 7)).cuda()
+    bounds = [(r * n // G, (r + 1) * n // G) for r in range(G)]
+    shards = [NavixEnv(env_id, e - b, seed=11, env_begin=b, num_envs_total=n) for b, e in bounds]
+    for s in shards:
+        s.reset()
+    again = NavixEnv(env_id, n, seed=11)
+    again.reset()
+    for t in range(steps):
+        o, r, te, tr = [x.clone() for x in full.step(acts[t])]
+        o2, r2, te2, tr2 = again.step(acts[t])
+        assert torch.equal(o, o2) and torch.equal(r, r2) and torch.equal(te, te2) and torch.equal(tr, tr2)
+        for s, (b, e) in zip(shards, bounds):
+            so, sr, ste, str_ = s.step(acts[t, b:e].contiguous())
+            assert torch.equal(so, o[b:e]) and torch.equal(sr, r[b:e])
+            assert torch.equal(ste, te[b:e]) and torch.equal(str_, tr[b:e])
+    tot = sum(s.stats().cpu() for s in shards)
+    assert torch.equal(tot, full.stats().cpu())
+    assert np.array_equal(np.concatenate([s.export_state() for s in shards]), full.export_state())
+
+
+def test_step_host_matches_device_path():
+    NavixEnv = navix()
+    n = 300
+    a = NavixEnv("DoorKey-8x8-v0", n, seed=4)
+    b = NavixEnv("DoorKey-8x8-v0", n, seed=4)
+    a.reset()
+    b.reset()
+    acts = random_actions(8, 50, n, 7)
+    h_obs = torch.empty((n, 7, 7, 3), dtype=torch.uint8).pin_memory()
+    h_rew = torch.empty(n, dtype=torch.float32).pin_memory()
+    h_te = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_tr = torch.empty(n, dtype=torch.uint8).pin_memory()
+    for t in range(50):
+        ha = torch.from_numpy(acts[t]).pin_memory()
+        a.step_host(ha, h_obs, h_rew, h_te, h_tr)
+        o, r, te, tr = b.step(ha.cuda())
+        assert torch.equal(h_obs, o.cpu()) and torch.equal(h_rew, r.cpu())
+        assert torch.equal(h_te, te.cpu()) and torch.equal(h_tr, tr.cpu())
+
+
+def test_unaligned_obs_buffer_uses_plain_stores():
+    NavixEnv = navix()
+    n = 256
+    a = NavixEnv("LavaGapS7-v0", n, seed=6)
+    b = NavixEnv("LavaGapS7-v0", n, seed=6)
+    big = torch.empty(n * 147 + 1, dtype=torch.uint8, device="cuda")
+    view = big[1:].view(n, 7, 7, 3)  # 1-byte offset: not 16-byte aligned
+    a.reset(out=view)
+    ref = b.reset()
+    assert torch.equal(view, ref)
+    acts = torch.from_numpy(random_actions(2, 30, n, 7)).cuda()
+    for t in range(30):
+        out = (view, torch.empty(n, device="cuda"), torch.empty(n, dtype=torch.uint8, device="cuda"),
+               torch.empty(n, dtype=torch.uint8, device="cuda"))
+        a.step(acts[t], out=out)
+        ro = b.step(acts[t])[0]
+        assert torch.equal(view, ro)
