@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libnavix.so")
 SOURCES = ["step_kernel.cu", "capi.cu"]
-HEADERS = ["layout.h", "philox.cuh", "levelgen.cuh", os.path.join("..", "..", "include", "navix.h")]
+HEADERS = ["layout.h", "philox.cuh", "levelgen.cuh", "obs.cuh", os.path.join("..", "..", "include", "navix.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,7 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-        with open(os.path.join(CSRC, src.replace(".cu", ".ptxas.txt")), "w") as f:
+        os.makedirs(os.path.join(HERE, "..", "build"), exist_ok=True)
+        with open(os.path.join(HERE, "..", "build", src.replace(".cu", ".ptxas.txt")), "w") as f:
             f.write(r.stderr)
         objs.append(obj)
     # default static cudart: the .so carries its own runtime, shares the

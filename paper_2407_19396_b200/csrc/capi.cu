@@ -135,6 +135,7 @@ KernelArgs make_args(navix_env* h) {
 
 navix_status launch(navix_env* h, int mode, KernelArgs& a, void* stream) {
   a.bulk_obs = (reinterpret_cast<uintptr_t>(a.obs) & 15u) == 0;
+  a.bulk_act = (reinterpret_cast<uintptr_t>(a.actions) & 15u) == 0;
   DeviceGuard dg(h->device);
   cudaError_t e = launch_env_kernel(h->cfg, mode, a, h->layout.n_tiles, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "navix kernel launch");
@@ -360,7 +361,7 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     return cuda_fail(e, "export D2H balls");
   uint8_t* o = static_cast<uint8_t*>(host);
   for (int64_t i = 0; i < h->n; ++i) {
-    const int64_t tile = i / TILE, lane = i % TILE;
+    const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
     uint8_t cells[8][8];
     for (int y = 0; y < c.height; ++y) {
       const uint64_t row = grid[(size_t)(tile * c.height + y) * TILE + lane];
@@ -368,13 +369,13 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     }
     if (c.family == FAM_DYNOBS)
       for (int b = 0; b < c.n_obstacles; ++b) {
-        const uint32_t p = (balls[i] >> (8 * b)) & 0xFF;
+        const uint32_t p = (balls[si] >> (8 * b)) & 0xFF;
         if (p) cells[p & 15][p >> 4] = make_cell(K_BALL, COL_BLUE);
       }
     uint8_t* p = o + (size_t)i * per;
     for (int y = 0; y < c.height; ++y)
       for (int x = 0; x < c.width; ++x, p += 3) from_cell(cells[y][x], p);
-    const uint64_t r = agent[i];
+    const uint64_t r = agent[si];
     p[0] = (uint8_t)r;
     p[1] = (uint8_t)(r >> 8);
     p[2] = (uint8_t)(r >> 16);
@@ -384,11 +385,11 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     p[4] = ct[1];
     p[5] = (uint8_t)(r >> 32);
     p[6] = (uint8_t)(r >> 40);
-    memcpy(p + 7, &episode[i], 4);
+    memcpy(p + 7, &episode[si], 4);
     p[11] = (uint8_t)((r >> 48) & 1);
     p += 12;
     for (int b = 0; b < c.n_obstacles; ++b, p += 2) {
-      const uint32_t q = (balls[i] >> (8 * b)) & 0xFF;
+      const uint32_t q = (balls[si] >> (8 * b)) & 0xFF;
       p[0] = (uint8_t)(q >> 4);
       p[1] = (uint8_t)(q & 15);
     }
@@ -450,16 +451,16 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
       const uint32_t q = (bl >> (8 * b)) & 0xFF;
       cells[q & 15][q >> 4] = CELL_EMPTY;
     }
-    const int64_t tile = i / TILE, lane = i % TILE;
+    const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
     for (int y = 0; y < H; ++y) {
       uint64_t row = 0;
       for (int x = 0; x < W; ++x) row |= (uint64_t)cells[y][x] << (8 * x);
       grid[(size_t)(tile * H + y) * TILE + lane] = row;
     }
-    agent[i] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
+    agent[si] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
                ((uint64_t)sc << 32) | ((uint64_t)pd << 48);
-    episode[i] = ep;
-    balls[i] = bl;
+    episode[si] = ep;
+    balls[si] = bl;
   }
   DeviceGuard dg(h->device);
   cudaError_t e = cudaDeviceSynchronize();

@@ -86,6 +86,11 @@ inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   return L;
 }
 
+// Tile-local env le <-> state slot (see step_kernel.cu): warp w lane l owns
+// env 4*l + w and slot 32*w + l.
+__host__ __device__ constexpr int slot_of_env(int le) { return (le & 3) * 32 + (le >> 2); }
+__host__ __device__ constexpr int env_of_slot(int slot) { return 4 * (slot & 31) + (slot >> 5); }
+
 // Kernel arguments (by value).
 struct KernelArgs {
   uint64_t* grid;
@@ -103,6 +108,7 @@ struct KernelArgs {
   uint32_t key_lo, key_hi;
   int reward_mode;
   int bulk_obs;         // 1: obs base is 16-B aligned -> cp.async.bulk store of full tiles
+  int bulk_act;         // 1: actions base is 16-B aligned -> cp.async.bulk load of full tiles
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2 };

@@ -1,0 +1,262 @@
+// obs.cuh — a6, the observation O = symbolic_first_person (Table 5),
+// MiniGrid's gen_obs_grid + process_vis + encode (R#10-R#14).
+//
+// Per env, all in registers + 16 SMEM line loads:
+//  1. view column vi (lateral offset vi-3) is a window of ONE world line
+//     (a row for dir 0/2, a column for dir 1/3) read with one 64-bit LDS;
+//     the shift and the byte reversal of the window are a single byte
+//     permute with a per-env selector (out-of-grid positions read arbitrary
+//     bytes: with a closed wall border they can never become visible, R#12).
+//  2. the 7x7 opacity matrix is gathered as 7 row masks (bit 7 of each cell).
+//  3. process_vis as 7 row closures.  Within a row the closure of the seeds
+//     is R(S) u L(S): R is the carry chain of T + (T & S) (carry into bit k =
+//     "k-1 visible and transparent"), L the same on bit-reversed rows; both
+//     run in one 32-bit add on [row | reversed row] with a stopper bit.
+//  4. invisible cells are zeroed, the visible ones SWAR-encoded 4 per word to
+//     (type, colour, state), and the 147-byte record is assembled with byte
+//     permutes at its final byte alignment, which is warp-uniform (a warp
+//     owns envs with equal index mod 4), then stored to SMEM word by word.
+#pragma once
+#include <cstdint>
+
+#include "layout.h"
+
+namespace navix {
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;  // default mode: selector nibble bit 3 replicates the sign of the byte
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// SWAR encode of 4 cell bytes (invisible cells already zeroed) to MiniGrid
+// (type, colour, state): kind >= 11 (closed 11 / locked 12 door) -> type 4,
+// state kind-10; otherwise type = kind, state 0; colour = bits 4-6.
+__device__ __forceinline__ void encode4(uint32_t w, uint32_t& ty, uint32_t& co, uint32_t& st) {
+  const uint32_t E = w & 0x0F0F0F0Fu;
+  co = (w >> 4) & 0x07070707u;
+  const uint32_t ge = (E + 0x05050505u) & 0x10101010u;
+  const uint32_t d = ge >> 4;
+  const uint32_t dm = ge - d;
+  ty = (E & ~dm) | (d << 2);
+  st = (E & dm) - d * 10u;
+}
+
+// ---------------------------------------------------------------- emission plan
+// A column's 21 record bytes (t c s for vj = 0..6) come from 6 registers:
+// 0: X00 = (t0 c0 t1 c1)  1: X01 = (t2 c2 t3 c3)  2: S0 = (s0 s1 s2 s3)
+// 3: X10 = (t4 c4 t5 c5)  4: X11 = (t6 c6 . .)     5: S1 = (s4 s5 s6 .)
+// and register 6 holds the pending partial word of the previous column.
+__host__ __device__ constexpr int col_reg(int i) {
+  return (i % 3 == 2) ? ((i / 3) / 4 ? 5 : 2) : ((i / 3) / 4) * 3 + ((i / 3) % 4) / 2;
+}
+__host__ __device__ constexpr int col_byte(int i) {
+  return (i % 3 == 2) ? (i / 3) % 4 : 2 * (((i / 3) % 4) % 2) + (i % 3);
+}
+
+struct WordPlan {
+  int ns;          // distinct sources (1..3)
+  int s0, s1, s2;  // source registers
+  uint32_t sel0;   // prmt(s0, s1, sel0)
+  uint32_t sel1;   // if ns == 3: prmt(tmp, s2, sel1)
+};
+
+// Output word k (from the word-aligned record base) of column VI at record
+// misalignment M.  Bytes before the column come from the pending word (reg 6),
+// bytes after it are don't-care (filled by the next column).
+__host__ __device__ constexpr WordPlan plan_word(int M, int VI, int k) {
+  int reg[4] = {-1, -1, -1, -1}, byt[4] = {0, 0, 0, 0};
+  const int O = M + 21 * VI;
+  for (int p = 0; p < 4; ++p) {
+    const int i = 4 * k + p - O;
+    if (i < 0) {
+      if (VI > 0) { reg[p] = 6; byt[p] = p; }
+    } else if (i <= 20) {
+      reg[p] = col_reg(i);
+      byt[p] = col_byte(i);
+    }
+  }
+  int src[3] = {-1, -1, -1}, ns = 0;
+  for (int p = 0; p < 4; ++p) {
+    if (reg[p] < 0) continue;
+    bool seen = false;
+    for (int q = 0; q < ns; ++q) seen = seen || src[q] == reg[p];
+    if (!seen) src[ns++] = reg[p];
+  }
+  WordPlan P{ns, src[0], src[1] < 0 ? src[0] : src[1], src[2], 0u, 0u};
+  uint32_t s0 = 0, s1 = 0;
+  for (int p = 0; p < 4; ++p) {
+    uint32_t n0 = 0, n1 = p;  // don't-care bytes: any index
+    if (reg[p] == src[0]) { n0 = byt[p]; n1 = p; }
+    else if (ns >= 2 && reg[p] == src[1]) { n0 = 4 + byt[p]; n1 = p; }
+    else if (ns == 3 && reg[p] == src[2]) { n0 = 0; n1 = 4 + byt[p]; }
+    s0 |= n0 << (4 * p);
+    s1 |= n1 << (4 * p);
+  }
+  P.sel0 = s0;
+  P.sel1 = s1;
+  return P;
+}
+
+// Stores bytes [p0, p1] of word v at SMEM word address w (p0 <= p1).
+__device__ __forceinline__ void sts_bytes(uint32_t* w, uint32_t v, int p0, int p1) {
+  uint8_t* b = reinterpret_cast<uint8_t*>(w);
+  if (p0 == 0 && p1 == 3) { *w = v; return; }
+  for (int p = p0; p <= p1;) {
+    if ((p & 1) == 0 && p + 1 <= p1) {
+      *reinterpret_cast<uint16_t*>(b + p) = (uint16_t)(v >> (8 * p));
+      p += 2;
+    } else {
+      b[p] = (uint8_t)(v >> (8 * p));
+      p += 1;
+    }
+  }
+}
+
+template <int M, int VI, int K>
+__device__ __forceinline__ void emit_word(uint32_t* out, const uint32_t (&r)[7], uint32_t& pend) {
+  constexpr WordPlan P = plan_word(M, VI, K);
+  uint32_t v;
+  if constexpr (P.ns == 3) {
+    const uint32_t t = prmt(r[P.s0], r[P.s1], P.sel0);
+    v = prmt(t, r[P.s2], P.sel1);
+  } else {
+    v = prmt(r[P.s0], r[P.s1], P.sel0);
+  }
+  constexpr int O = M + 21 * VI;
+  constexpr int first = 4 * K, last = 4 * K + 3;   // stream bytes covered by word K
+  constexpr int col_end = O + 20;                  // last stream byte of this column
+  constexpr int rec_end = M + 146;                 // last stream byte of the record
+  if constexpr (last <= col_end) {
+    // word complete: store (partially if it starts before the record)
+    if constexpr (first < M) sts_bytes(out + K, v, M, 3);
+    else *(out + K) = v;
+  } else if constexpr (col_end == rec_end) {
+    sts_bytes(out + K, v, 0, col_end - first);   // record tail
+  } else {
+    pend = v;                                      // continues in the next column
+  }
+}
+
+template <int M, int VI>
+__device__ __forceinline__ void emit_column(uint32_t* out, const uint32_t (&r)[7], uint32_t& pend) {
+  constexpr int O = M + 21 * VI;
+  constexpr int K0 = O / 4, K1 = (O + 20) / 4;
+  emit_word<M, VI, K0>(out, r, pend);
+  emit_word<M, VI, K0 + 1>(out, r, pend);
+  emit_word<M, VI, K0 + 2>(out, r, pend);
+  emit_word<M, VI, K0 + 3>(out, r, pend);
+  emit_word<M, VI, K0 + 4>(out, r, pend);
+  if constexpr (K1 >= K0 + 5) emit_word<M, VI, K0 + 5>(out, r, pend);
+}
+
+template <int M>
+__device__ __forceinline__ void emit_record(uint32_t* out, uint32_t (&r)[7][7]) {
+  uint32_t pend = 0;
+  r[0][6] = pend;
+  emit_column<M, 0>(out, r[0], pend);
+  r[1][6] = pend;
+  emit_column<M, 1>(out, r[1], pend);
+  r[2][6] = pend;
+  emit_column<M, 2>(out, r[2], pend);
+  r[3][6] = pend;
+  emit_column<M, 3>(out, r[3], pend);
+  r[4][6] = pend;
+  emit_column<M, 4>(out, r[4], pend);
+  r[5][6] = pend;
+  emit_column<M, 5>(out, r[5], pend);
+  r[6][6] = pend;
+  emit_column<M, 6>(out, r[6], pend);
+}
+
+__device__ __forceinline__ void encode_col(uint32_t c_lo, uint32_t c_hi, uint32_t m_lo, uint32_t m_hi, uint32_t pend,
+                                           uint32_t (&r)[7]) {
+  uint32_t ty, co, st;
+  encode4(c_lo & m_lo, ty, co, st);
+  r[0] = prmt(ty, co, 0x5140);  // t0 c0 t1 c1
+  r[1] = prmt(ty, co, 0x7362);  // t2 c2 t3 c3
+  r[2] = st;
+  encode4(c_hi & m_hi, ty, co, st);
+  r[3] = prmt(ty, co, 0x5140);
+  r[4] = prmt(ty, co, 0x7362);
+  r[5] = st;
+  r[6] = pend;
+}
+
+// Observation of one env.  rows/cols: this env's 8 SMEM row / column lines
+// (stride TILE); out: word-aligned SMEM address at or before its record,
+// whose first byte is at misalignment M (warp-uniform, 0..3).  All 7 columns
+// are encoded first; only the emission is specialised on M (one warp-uniform
+// switch), so the four variants share the rest of the code.
+__device__ __forceinline__ void observe_emit(const uint64_t* rows, const uint64_t* cols, int ax, int ay, int dir,
+                                             uint32_t carry, uint32_t* out, int M) {
+  // view column vi <-> world line parallel to the facing direction (P6 pin):
+  //  dir 0: row    ay+vi-3, x = ax+6-vj     dir 1: column ax+3-vi, y = ay+6-vj
+  //  dir 2: row    ay+3-vi, x = ax-6+vj     dir 3: column ax+vi-3, y = ay-6+vj
+  const bool odd = dir & 1;
+  const uint64_t* lines = odd ? cols : rows;
+  const int base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
+  const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
+  const int s = (dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6) & 7;
+  const bool rev = dir <= 1;
+  const uint32_t s4 = (uint32_t)s * 0x1111u;
+  // byte selectors: cell vj of the column = line byte (s + vj) or (s + 6 - vj), mod 8
+  const uint32_t sel_lo = (s4 + (rev ? 0x3456u : 0x3210u)) & 0x7777u;
+  const uint32_t sel_hi = (s4 + (rev ? 0x0012u : 0x7654u)) & 0x7777u;
+  uint32_t clo[7], chi[7];
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    const uint64_t line = lines[((base + sgn * vi) & 7) * TILE];
+    const uint32_t lo = (uint32_t)line, hi = (uint32_t)(line >> 32);
+    clo[vi] = prmt(lo, hi, sel_lo);
+    chi[vi] = prmt(lo, hi, sel_hi);
+  }
+  // opacity rows: byte vj of op has bit vi set iff cell (vi, vj) is opaque
+  uint32_t op_lo = 0, op_hi = 0;
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    op_lo |= (clo[vi] >> (7 - vi)) & (0x01010101u << vi);
+    op_hi |= (chi[vi] >> (7 - vi)) & (0x01010101u << vi);
+  }
+  // transparency rows and their 7-bit reversals (bit vi -> bit 6-vi)
+  const uint32_t t_lo = ~op_lo & 0x7F7F7F7Fu, t_hi = ~op_hi & 0x7F7F7F7Fu;
+  const uint32_t tr_lo = (prmt(__brev(t_lo), 0u, 0x0123u) >> 1) & 0x7F7F7F7Fu;
+  const uint32_t tr_hi = (prmt(__brev(t_hi), 0u, 0x0123u) >> 1) & 0x7F7F7F7Fu;
+  // rows vj = 6 .. 0 ([MG] process_vis order): V = R(S) | L(S), computed as
+  // one carry chain on X = S | rev(S) << 8 over T2 = T | rev(T) << 8 (bit 7 = 0
+  // stops the carry between the halves)
+  uint32_t vis_lo = 0, vis_hi = 0;
+  uint32_t seed = 1u << 3;
+#pragma unroll
+  for (int j = 6; j >= 0; --j) {
+    const uint32_t tw = j < 4 ? t_lo : t_hi, trw = j < 4 ? tr_lo : tr_hi;
+    const uint32_t b = (uint32_t)(j & 3);
+    const uint32_t t2 = prmt(tw, trw, 0x4400u | ((4u + b) << 4) | b) & 0x7F7Fu;  // byte0 = t, byte1 = rev t
+    const uint32_t t = t2 & 0x7Fu;
+    const uint32_t x = seed | ((__brev(seed) >> 25) << 8);
+    const uint32_t tx = t2 & x;
+    const uint32_t v2 = x | ((t2 + tx) ^ t2 ^ tx);
+    const uint32_t v = (v2 | (__brev(v2 >> 8) >> 25)) & 0x7Fu;
+    const uint32_t av = v & t;
+    seed = (av | (av << 1) | (av >> 1)) & 0x7Fu;
+    if (j < 4) vis_lo |= v << (8 * j);
+    else vis_hi |= v << (8 * (j - 4));
+  }
+  // the agent sees what it carries (R#13): view cell (3, 6), always visible
+  chi[3] = prmt(chi[3], carry, 0x3410u);
+  uint32_t r[7][7];
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    const uint32_t m_lo = prmt(vis_lo << (7 - vi), 0u, 0xBA98u);
+    const uint32_t m_hi = prmt(vis_hi << (7 - vi), 0u, 0xBA98u);
+    encode_col(clo[vi], chi[vi], m_lo, m_hi, 0u, r[vi]);
+  }
+  switch (M) {  // one warp-uniform dispatch for the whole record
+    case 0: emit_record<0>(out, r); break;
+    case 1: emit_record<1>(out, r); break;
+    case 2: emit_record<2>(out, r); break;
+    default: emit_record<3>(out, r); break;
+  }
+}
+
+}  // namespace navix

@@ -25,6 +25,7 @@
 
 #include "layout.h"
 #include "levelgen.cuh"
+#include "obs.cuh"
 #include "philox.cuh"
 
 namespace navix {
@@ -32,6 +33,29 @@ namespace navix {
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// mbarrier + TMA bulk copy (global -> shared) primitives
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(mbar)
+               : "memory");
 }
 
 // 8x8 byte transpose: rows r[y] (byte x) -> cols c[x] (byte y), 32 byte permutes.
@@ -66,150 +90,7 @@ __device__ __forceinline__ void build_cols(const uint64_t* rows, uint64_t* cols)
   }
 }
 
-// SWAR encode of 4 cells: (type, colour, state) bytes, masked by visibility.
-__device__ __forceinline__ void encode4(uint32_t w, uint32_t m, uint32_t& ty, uint32_t& co, uint32_t& st) {
-  const uint32_t E = w & 0x0F0F0F0Fu;
-  co = ((w >> 4) & 0x07070707u) & m;
-  const uint32_t ge = (E + 0x05050505u) & 0x10101010u;  // kind >= 11: closed / locked door
-  const uint32_t d = ge >> 4;
-  const uint32_t dm = ge - d;                            // 0x0F per door byte
-  ty = ((E & ~dm) | (d << 2)) & m;                       // doors -> 4
-  st = ((E & dm) - d * 10u) & m;                         // 11 -> 1, 12 -> 2
-}
-
-// Interleave 4 cells' (t, c, s) bytes into 12 bytes (3 words).
-__device__ __forceinline__ void interleave4(uint32_t ty, uint32_t co, uint32_t st, uint32_t& q0, uint32_t& q1,
-                                            uint32_t& q2) {
-  const uint32_t x0 = __byte_perm(ty, co, 0x5140);  // t0 c0 t1 c1
-  const uint32_t x1 = __byte_perm(ty, co, 0x7362);  // t2 c2 t3 c3
-  q0 = __byte_perm(x0, st, 0x2410);                 // t0 c0 s0 t1
-  const uint32_t y = __byte_perm(x0, st, 0x0053);   // c1 s1 .  .
-  q1 = __byte_perm(y, x1, 0x5410);                  // c1 s1 t2 c2
-  q2 = __byte_perm(x1, st, 0x7326);                 // s2 t3 c3 s3
-}
-
-// Place the 21-byte column VI at byte 21*VI of the 147-byte record.
-template <int VI>
-__device__ __forceinline__ void emit_column(uint32_t (&rec)[37], const uint32_t (&w)[6]) {
-  constexpr int O = 21 * VI, B = O / 4, R = O % 4;
-  if constexpr (R == 0) {
-#pragma unroll
-    for (int k = 0; k < 6; ++k) rec[B + k] = w[k];
-  } else {
-    rec[B] |= w[0] << (8 * R);
-#pragma unroll
-    for (int k = 1; k < 6; ++k) rec[B + k] = __funnelshift_l(w[k - 1], w[k], 8 * R);
-  }
-}
-
-// The egocentric view column VI (lateral offset VI-3) as 7 cell bytes
-// (byte vj = distance 6-vj from the agent): a window of one world line.
-struct ViewGeom {
-  const uint64_t* lines;  // &s_rows[0][tid] or &s_cols[0][tid]
-  int base, sgn, nlines, shift, rev;
-};
-
-__device__ __forceinline__ uint64_t view_column(const ViewGeom& g, int vi) {
-  const int L = g.base + g.sgn * vi;
-  uint64_t line = 0;
-  if ((unsigned)L < (unsigned)g.nlines) line = g.lines[L * TILE];
-  uint64_t wv = g.shift >= 0 ? (line >> (8 * g.shift)) : (line << (-8 * g.shift));
-  wv &= 0x00FFFFFFFFFFFFFFull;
-  const uint32_t lo = (uint32_t)wv, hi = (uint32_t)(wv >> 32);
-  const uint64_t rv = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32 | __byte_perm(hi, 0, 0x0123)) >> 8;
-  return g.rev ? rv : wv;
-}
-
-template <int VI>
-__device__ __forceinline__ void encode_column(uint32_t (&rec)[37], uint64_t colv, uint64_t vis) {
-  const uint64_t m = ((vis >> VI) & 0x0101010101010101ull) * 0xFFull;
-  uint32_t ty, co, st, w[6];
-  encode4((uint32_t)colv, (uint32_t)m, ty, co, st);
-  interleave4(ty, co, st, w[0], w[1], w[2]);
-  encode4((uint32_t)(colv >> 32), (uint32_t)(m >> 32), ty, co, st);
-  uint32_t unused;
-  interleave4(ty, co, st, w[3], w[4], unused);
-  w[5] = (st >> 16) & 0xFFu;  // s6
-  emit_column<VI>(rec, w);
-}
-
-// a6: the 147-byte observation of one env (Table 5, [MG] gen_obs).
-template <int H, int W>
-__device__ __forceinline__ void observe(const uint64_t* rows, const uint64_t* cols, int ax, int ay, int dir,
-                                        uint8_t carry, uint32_t (&rec)[37]) {
-  // view column vi <-> world line parallel to the facing direction:
-  //  dir 0 (east):  row    ay+vi-3, x = ax+6-vj  (reversed window from ax)
-  //  dir 1 (south): column ax+3-vi, y = ay+6-vj  (reversed window from ay)
-  //  dir 2 (west):  row    ay+3-vi, x = ax-6+vj  (window from ax-6)
-  //  dir 3 (north): column ax+vi-3, y = ay-6+vj  (window from ay-6)
-  ViewGeom g;
-  const bool odd = dir & 1;
-  g.lines = odd ? cols : rows;
-  g.nlines = odd ? W : H;
-  g.base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
-  g.sgn = (dir == 0 || dir == 3) ? 1 : -1;
-  g.shift = dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6;
-  g.rev = dir <= 1;
-  uint64_t col[7];
-#pragma unroll
-  for (int vi = 0; vi < 7; ++vi) col[vi] = view_column(g, vi);
-  // opacity rows: byte vj of OP has bit vi set iff view cell (vi, vj) is opaque
-  uint64_t op = 0;
-#pragma unroll
-  for (int vi = 0; vi < 7; ++vi) op |= (col[vi] & 0x8080808080808080ull) >> (7 - vi);
-  // [MG] process_vis: rows vj = 6 .. 0; within a row the visible set is the
-  // closure of the seeds; a rightward closure is the carry chain of
-  // T + (T & S) (carry into bit k = "k-1 visible and transparent"), the
-  // leftward one the same on bit-reversed rows.
-  uint64_t vis = 0;
-  uint32_t seed = 1u << 3;
-#pragma unroll
-  for (int j = 6; j >= 0; --j) {
-    const uint32_t t = ~(uint32_t)(op >> (8 * j)) & 0x7Fu;
-    uint32_t ts = t & seed;
-    uint32_t v = (seed | ((t + ts) ^ t ^ ts)) & 0x7Fu;
-    const uint32_t tr = __brev(t) >> 25;
-    uint32_t vr = __brev(v) >> 25;
-    ts = tr & vr;
-    vr = (vr | ((tr + ts) ^ tr ^ ts)) & 0x7Fu;
-    v = __brev(vr) >> 25;
-    const uint32_t a = v & t;
-    seed = (a | (a << 1) | (a >> 1)) & 0x7Fu;
-    vis |= (uint64_t)v << (8 * j);
-  }
-  // the agent sees what it carries (R#13): view cell (3, 6)
-  col[3] = (col[3] & ~(0xFFull << 48)) | ((uint64_t)carry << 48);
-  encode_column<0>(rec, col[0], vis);
-  encode_column<1>(rec, col[1], vis);
-  encode_column<2>(rec, col[2], vis);
-  encode_column<3>(rec, col[3], vis);
-  encode_column<4>(rec, col[4], vis);
-  encode_column<5>(rec, col[5], vis);
-  encode_column<6>(rec, col[6], vis);
-}
-
-// Store the 147-byte record at byte tid*147 of the SMEM staging buffer.
-__device__ __forceinline__ void stage_obs(uint8_t* s_obs, int tid, const uint32_t (&rec)[37]) {
-  const uint32_t off = (uint32_t)tid * OBS_BYTES;
-  const uint32_t m = off & 3u, sh = 8u * m;
-  uint32_t* s32 = reinterpret_cast<uint32_t*>(s_obs) + (off >> 2);
-  uint8_t* s8 = reinterpret_cast<uint8_t*>(s32);
-  const uint32_t first = rec[0] << sh;
-  if (m == 0) s32[0] = first;
-  else if (m == 1) { s8[1] = (uint8_t)(first >> 8); *reinterpret_cast<uint16_t*>(s8 + 2) = (uint16_t)(first >> 16); }
-  else if (m == 2) *reinterpret_cast<uint16_t*>(s8 + 2) = (uint16_t)(first >> 16);
-  else s8[3] = (uint8_t)(first >> 24);
-#pragma unroll
-  for (int j = 1; j < 36; ++j) s32[j] = __funnelshift_l(rec[j - 1], rec[j], sh);
-  const uint32_t w36 = __funnelshift_l(rec[35], rec[36], sh);
-  if (m >= 1) s32[36] = w36;
-  else { *reinterpret_cast<uint16_t*>(s8 + 144) = (uint16_t)w36; s8[146] = (uint8_t)(w36 >> 16); }
-  const uint32_t w37 = __funnelshift_l(rec[36], 0u, sh);
-  if (m == 2) s8[148] = (uint8_t)w37;
-  else if (m == 3) *reinterpret_cast<uint16_t*>(s8 + 148) = (uint16_t)w37;
-}
-
-__device__ __forceinline__ float success_reward(int mode, uint32_t sc, uint32_t T) {
+__device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) {
   if (mode == 1) return 1.0f;
   // R#2: binary64, [MG] order, no contraction, one rounding to binary32
   const double q = __ddiv_rn((double)sc, (double)T);
@@ -218,35 +99,68 @@ __device__ __forceinline__ float success_reward(int mode, uint32_t sc, uint32_t 
 }
 
 // ------------------------------------------------------------------ kernel
+// Lane <-> env mapping inside a tile: thread tid = 32*w + l (warp w, lane l)
+// owns tile-local env le = 4*l + w.  All state arrays are indexed by the
+// "slot" tid, so every warp access to them is contiguous; caller arrays
+// (actions, obs, reward, flags) are indexed by the env.  A warp's envs then
+// share le mod 4, so their 147-byte records start at the same byte
+// misalignment M = 147*le mod 4 = 3w mod 4 and the record emission is
+// specialised per warp at compile time (no per-lane shifts, and the
+// per-lane SMEM word stride 147 is odd: bank-conflict free).
 template <int FAM, int H, int W, int MODE>
 __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
   using C = Cfg<FAM, H, W>;
   __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
-  __shared__ __align__(16) uint64_t s_rows[H][TILE];
-  __shared__ __align__(16) uint64_t s_cols[W][TILE];
-  __shared__ unsigned int s_any;
+  __shared__ __align__(16) uint64_t s_rows[8][TILE];
+  __shared__ __align__(16) uint64_t s_cols[8][TILE];
+  __shared__ __align__(16) uint64_t s_agent[TILE];
+  __shared__ __align__(16) uint32_t s_balls[FAM == FAM_DYNOBS ? TILE : 4];
+  __shared__ __align__(16) uint32_t s_episode[FAM == FAM_DYNOBS ? TILE : 4];
+  __shared__ __align__(16) uint8_t s_act[TILE];
+  __shared__ __align__(8) uint64_t s_mbar;
 
   const int tid = threadIdx.x;
-  const int64_t e = (int64_t)blockIdx.x * TILE + tid;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int le = 4 * lane + warp;
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  const int64_t slot = tile0 + tid;   // state index
+  const int64_t e = tile0 + le;       // env index (caller arrays)
   const bool valid = e < a.n;
-  const uint32_t genv = a.env_begin + (uint32_t)e;
+  const uint32_t genv = a.env_begin + (uint32_t)e;  // global env index: Philox counter word c0
   uint64_t* const rows = &s_rows[0][tid];
   uint64_t* const cols = &s_cols[0][tid];
   RowView g{rows};
 
-  // ---- a1: stage
+  // ---- a1: stage: one TMA bulk copy per array brings the tile's grid rows,
+  // agent records and actions (and DynObs balls / episode counters) into SMEM
   uint8_t act = 0;
   uint64_t rec = 0;
   uint32_t balls = 0, episode = 0;
   if (MODE != MODE_RESET) {
-    const uint64_t* gsrc = a.grid + (int64_t)blockIdx.x * H * TILE + tid;
-#pragma unroll
-    for (int y = 0; y < H; ++y) rows[y * TILE] = gsrc[y * TILE];
-    rec = a.agent[e];
-    if (MODE == MODE_STEP && valid) act = a.actions[e];
+    const bool full = tile0 + TILE <= a.n;
+    const bool act_bulk = MODE == MODE_STEP && a.bulk_act && full;
+    const uint32_t mbar = smem_u32(&s_mbar);
+    if (tid == 0) {
+      mbar_init(mbar, 1);
+      const uint32_t bytes = H * TILE * 8 + TILE * 8 + (act_bulk ? TILE : 0) +
+                             (FAM == FAM_DYNOBS ? (MODE == MODE_STEP ? 8 : 4) * TILE : 0);
+      mbar_expect_tx(mbar, bytes);
+      bulk_g2s(&s_rows[0][0], a.grid + tile0 * H, H * TILE * 8, mbar);
+      bulk_g2s(s_agent, a.agent + tile0, TILE * 8, mbar);
+      if (act_bulk) bulk_g2s(s_act, a.actions + tile0, TILE, mbar);
+      if (FAM == FAM_DYNOBS) {
+        bulk_g2s(s_balls, a.balls + tile0, TILE * 4, mbar);
+        if (MODE == MODE_STEP) bulk_g2s(s_episode, a.episode + tile0, TILE * 4, mbar);
+      }
+    }
+    if (MODE == MODE_STEP && !act_bulk && valid) act = a.actions[e];
+    __syncthreads();  // mbarrier initialised before anyone waits on it
+    mbar_wait(mbar, 0);
+    rec = s_agent[tid];
+    if (act_bulk) act = s_act[le];
     if (FAM == FAM_DYNOBS) {
-      balls = a.balls[e];
-      if (MODE == MODE_STEP) episode = a.episode[e];
+      balls = s_balls[tid];
+      if (MODE == MODE_STEP) episode = s_episode[tid];
     }
   }
   int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
@@ -263,7 +177,7 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
   if (regen) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
     if (MODE == MODE_STEP) {
-      if (FAM != FAM_DYNOBS) episode = a.episode[e];
+      if (FAM != FAM_DYNOBS) episode = a.episode[slot];
       episode += 1;
     }
     const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi);
@@ -315,60 +229,41 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
           }
         }
       }
-      // ---- a4: intervention I (Table 3; [MG] MiniGridEnv.step)
+      // ---- a4: intervention I (Table 3; [MG] MiniGridEnv.step), branch-free:
+      // every action's effect is computed with selects so a warp never splits
+      // on the action value.
       sc += 1;
       uint8_t* fp = g.at(fx, fy);
-      const uint8_t fc = *fp;
+      const uint32_t fc = *fp;
       const uint32_t kind = fc & 15u;
-      bool success = false, lava = false, coll = false;
-      switch (act) {
-        case 0: dir = (dir + 3) & 3; break;
-        case 1: dir = (dir + 1) & 3; break;
-        case 2:
-          if ((0x31Au >> kind) & 1u) { ax = fx; ay = fy; }  // empty, floor, open door, goal, lava
-          success = kind == K_GOAL;
-          lava = kind == K_LAVA;
-          break;
-        case 3:
-          if (((0xE0u >> kind) & 1u) && carry == CELL_EMPTY) {  // key, ball, box
-            carry = fc;
-            *fp = CELL_EMPTY;
-            grid_dirty = true;
-          }
-          break;
-        case 4:
-          if (fc == CELL_EMPTY && carry != CELL_EMPTY) {
-            *fp = carry;
-            carry = CELL_EMPTY;
-            grid_dirty = true;
-          }
-          break;
-        case 5: {
-          const uint8_t col = (fc >> 4) & 7;
-          if (kind == K_DOOR_LOCKED) {
-            if ((carry & 15) == K_KEY && ((carry >> 4) & 7) == col) {
-              *fp = make_cell(K_DOOR_OPEN, col);
-              grid_dirty = true;
-            }
-          } else if (kind == K_DOOR_CLOSED) {
-            *fp = make_cell(K_DOOR_OPEN, col);
-            grid_dirty = true;
-          } else if (kind == K_DOOR_OPEN) {
-            *fp = make_cell(K_DOOR_CLOSED, col);
-            grid_dirty = true;
-          } else if (kind == K_BOX) {
-            *fp = CELL_EMPTY;
-            grid_dirty = true;
-          }
-          break;
-        }
-        default: break;  // done, and out-of-range actions (R#15)
+      const bool is_fwd = act == 2, is_pick = act == 3, is_drop = act == 4, is_tog = act == 5;
+      dir = (dir + (act == 1 ? 1 : 0) + (act == 0 ? 3 : 0)) & 3;
+      const bool walk = (0x31Au >> kind) & 1u;  // empty, floor, open door, goal, lava
+      ax = (is_fwd && walk) ? fx : ax;
+      ay = (is_fwd && walk) ? fy : ay;
+      bool success = is_fwd && kind == K_GOAL;
+      const bool lava = is_fwd && kind == K_LAVA;
+      bool coll = false;
+      const bool pick = is_pick && ((0xE0u >> kind) & 1u) && carry == CELL_EMPTY;  // key, ball, box
+      const bool drop = is_drop && fc == CELL_EMPTY && carry != CELL_EMPTY;
+      // [MG] Door.toggle / Box.toggle
+      const uint32_t colbits = fc & 0x70u;
+      const bool key_ok = (carry & 15u) == K_KEY && (carry & 0x70u) == colbits;
+      const uint32_t opened = colbits | K_DOOR_OPEN, closed = OPAQUE_BIT | colbits | K_DOOR_CLOSED;
+      const uint32_t tog = ((kind == K_DOOR_LOCKED && key_ok) || kind == K_DOOR_CLOSED) ? opened
+                           : kind == K_DOOR_OPEN ? closed
+                           : kind == K_BOX ? (uint32_t)CELL_EMPTY : fc;
+      const uint32_t newf = pick ? (uint32_t)CELL_EMPTY : drop ? (uint32_t)carry : is_tog ? tog : fc;
+      carry = pick ? (uint8_t)fc : drop ? CELL_EMPTY : carry;
+      if (newf != fc) {
+        *fp = (uint8_t)newf;
+        grid_dirty = true;
       }
-      if (FAM == FAM_KEYCORRIDOR && act == 3 && (carry & 15) == K_BALL) success = true;  // R#8
-      if (FAM == FAM_DYNOBS && act == 2 && not_clear) { coll = true; success = false; }  // R#4
+      if (FAM == FAM_KEYCORRIDOR && is_pick && (carry & 15) == K_BALL) success = true;  // R#8
+      if (FAM == FAM_DYNOBS && is_fwd && not_clear) { coll = true; success = false; }  // R#4
       // ---- a5: reward and termination (Eq. 1, Tables 6-7)
       if (coll) reward = -1.0f;
-      else if (success) reward = success_reward(a.reward_mode, sc, C::T);
+      else if (__builtin_expect(success, 0)) reward = success_reward(a.reward_mode, sc, C::T);
       else if (lava) reward = a.reward_mode == 1 ? -1.0f : 0.0f;
       term = success || lava || coll;
       trunc = sc >= (uint32_t)C::T && !term;
@@ -385,29 +280,31 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
     }
   }
 
-  // ---- a6: observation
+  // ---- a6: observation (obs.cuh)
   build_cols<H, W>(rows, cols);
-  uint32_t obsrec[37];
-  observe<H, W>(rows, cols, ax, ay, dir, carry, obsrec);
-  stage_obs(s_obs, tid, obsrec);
+  {
+    uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
+    const int rec_byte = le * OBS_BYTES;
+    const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
+    observe_emit(rows, cols, ax, ay, dir, carry, s32 + ((rec_byte - M) >> 2), M);
+  }
 
   // ---- a7: stores
-  const int64_t tile_env0 = (int64_t)blockIdx.x * TILE;
-  const int64_t nvalid64 = a.n - tile_env0;
+  const int64_t nvalid64 = a.n - tile0;
   const int nvalid = nvalid64 >= TILE ? TILE : (int)nvalid64;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   const bool bulk = a.bulk_obs && nvalid == TILE;
   if (bulk) {
     if (tid == 0) {
-      uint8_t* dst = a.obs + tile_env0 * OBS_BYTES;
+      uint8_t* dst = a.obs + tile0 * OBS_BYTES;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                    "r"(smem_u32(s_obs)), "r"((uint32_t)(TILE * OBS_BYTES))
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   } else {
-    uint8_t* dst = a.obs + tile_env0 * OBS_BYTES;
+    uint8_t* dst = a.obs + tile0 * OBS_BYTES;
     for (int i = tid; i < nvalid * OBS_BYTES; i += TILE) dst[i] = s_obs[i];
   }
 
@@ -420,12 +317,12 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
       }
       const uint64_t nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) |
                             ((uint64_t)carry << 24) | ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48);
-      a.agent[e] = nrec;
-      if (regen) a.episode[e] = episode;
-      if (FAM == FAM_DYNOBS) a.balls[e] = balls;
+      a.agent[slot] = nrec;
+      if (regen) a.episode[slot] = episode;
+      if (FAM == FAM_DYNOBS) a.balls[slot] = balls;
     }
     if (grid_dirty) {
-      uint64_t* gdst = a.grid + (int64_t)blockIdx.x * H * TILE + tid;
+      uint64_t* gdst = a.grid + tile0 * H + tid;
 #pragma unroll
       for (int y = 0; y < H; ++y)
         gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : rows[y * TILE];
@@ -439,11 +336,11 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
                          st_lava * vv, st_coll * vv, st_trunc * vv, st_fail * vv};
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
-        if ((tid & 31) == 0) {
-          unsigned long long* slot = a.stats + (size_t)((blockIdx.x * (TILE / 32) + (tid >> 5)) % NSLOT) * 8;
+        if (lane == 0) {
+          unsigned long long* st = a.stats + (size_t)((blockIdx.x * (TILE / 32) + warp) % NSLOT) * 8;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            if (v[k]) atomicAdd(slot + k, (unsigned long long)v[k]);
+            if (v[k]) atomicAdd(st + k, (unsigned long long)v[k]);
         }
       }
     }
