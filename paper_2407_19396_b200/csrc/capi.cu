@@ -125,6 +125,7 @@ KernelArgs make_args(navix_env* h) {
   a.episode = reinterpret_cast<uint32_t*>(s + h->layout.episode_off);
   a.balls = reinterpret_cast<uint32_t*>(s + h->layout.balls_off);
   a.stats = reinterpret_cast<unsigned long long*>(s + h->layout.stats_off);
+  a.sched = reinterpret_cast<unsigned int*>(s + h->layout.sched_off);
   a.n = h->n;
   a.env_begin = (uint32_t)h->env_begin;
   a.key_lo = (uint32_t)h->seed;
@@ -241,6 +242,15 @@ navix_status navix_create_shard(const char* env_id, int64_t num_envs_total, int6
     }
     h->owns_state = true;
   }
+  {  // scheduler and statistics start at zero even before the first reset
+    DeviceGuard dg(device);
+    e = cudaMemset(h->state + h->layout.stats_off, 0, h->layout.total - h->layout.stats_off);
+    if (e != cudaSuccess) {
+      if (h->owns_state) cudaFree(h->state);
+      delete h;
+      return cuda_fail(e, "cudaMemset(stats)");
+    }
+  }
   *out = h;
   return NAVIX_OK;
 }
@@ -256,7 +266,8 @@ navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream) {
   if (!h || !obs) return fail(NAVIX_E_INVALID_ARG, "navix_reset: null handle or obs");
   {
     DeviceGuard dg(h->device);
-    cudaError_t e = cudaMemsetAsync(h->state + h->layout.stats_off, 0, (size_t)NSLOT * 64, (cudaStream_t)stream);
+    cudaError_t e = cudaMemsetAsync(h->state + h->layout.stats_off, 0, h->layout.total - h->layout.stats_off,
+                                    (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(stats)");
   }
   KernelArgs a = make_args(h);

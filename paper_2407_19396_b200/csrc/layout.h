@@ -7,6 +7,7 @@
 //   episode u32 [n_pad]               episode counter (counter word c1, R#20)
 //   balls   u32 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b
 //   stats   u64 [NSLOT][8]            striped int64 episode statistics
+//   sched   u32 [2]                   persistent step kernel tile scheduler
 // n_pad = num_envs rounded up to TILE.  The struct-of-arrays "row plane"
 // layout makes every warp load of a grid row one contiguous 256-byte segment
 // and lets the kernel fetch a whole world row with one 64-bit load.
@@ -62,7 +63,7 @@ struct EnvConfig {
 // Byte offsets of the arrays inside one state allocation.
 struct StateLayout {
   int64_t n_pad, n_tiles;
-  size_t grid_off, agent_off, episode_off, balls_off, stats_off, total;
+  size_t grid_off, agent_off, episode_off, balls_off, stats_off, sched_off, total;
 };
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -82,6 +83,8 @@ inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   off = align_up(off + (c.family == FAM_DYNOBS ? (size_t)L.n_pad * 4 : 0), 256);
   L.stats_off = off;
   off = align_up(off + (size_t)NSLOT * 8 * 8, 256);
+  L.sched_off = off;
+  off = align_up(off + 2 * sizeof(unsigned int), 256);
   L.total = off;
   return L;
 }
@@ -98,6 +101,7 @@ struct KernelArgs {
   uint32_t* episode;
   uint32_t* balls;
   unsigned long long* stats;
+  unsigned int* sched;  // persistent tile scheduler {next tile, CTAs done}
   const uint8_t* actions;
   uint8_t* obs;
   float* reward;

@@ -183,18 +183,16 @@ __device__ __forceinline__ void encode_col(uint32_t c_lo, uint32_t c_hi, uint32_
   r[6] = pend;
 }
 
-// Observation of one env.  rows/cols: this env's 8 SMEM row / column lines
-// (stride TILE); out: word-aligned SMEM address at or before its record,
+// Observation of one env.  lines: this env's 8 SMEM lines (stride TILE):
+// its grid rows when dir is even, its grid columns when dir is odd; out: word-aligned SMEM address at or before its record,
 // whose first byte is at misalignment M (warp-uniform, 0..3).  All 7 columns
 // are encoded first; only the emission is specialised on M (one warp-uniform
 // switch), so the four variants share the rest of the code.
-__device__ __forceinline__ void observe_emit(const uint64_t* rows, const uint64_t* cols, int ax, int ay, int dir,
-                                             uint32_t carry, uint32_t* out, int M) {
+__device__ __forceinline__ void observe_emit(const uint64_t* lines, int ax, int ay, int dir, uint32_t carry,
+                                             uint32_t* out, int M) {
   // view column vi <-> world line parallel to the facing direction (P6 pin):
   //  dir 0: row    ay+vi-3, x = ax+6-vj     dir 1: column ax+3-vi, y = ay+6-vj
   //  dir 2: row    ay+3-vi, x = ax-6+vj     dir 3: column ax+vi-3, y = ay-6+vj
-  const bool odd = dir & 1;
-  const uint64_t* lines = odd ? cols : rows;
   const int base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
   const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
   const int s = (dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6) & 7;

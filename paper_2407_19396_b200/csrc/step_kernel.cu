@@ -51,6 +51,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint32_t mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(smem)),
@@ -58,7 +62,8 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
                : "memory");
 }
 
-// 8x8 byte transpose: rows r[y] (byte x) -> cols c[x] (byte y), 32 byte permutes.
+// 8x8 byte transpose of one env's lines in place: rows (byte x of line y) ->
+// columns (byte y of line x), 32 byte permutes.
 __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t& o0,
                                              uint32_t& o1, uint32_t& o2, uint32_t& o3) {
   const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
@@ -69,12 +74,11 @@ __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t 
   o3 = __byte_perm(t2, t3, 0x7632);
 }
 
-template <int H, int W>
-__device__ __forceinline__ void build_cols(const uint64_t* rows, uint64_t* cols) {
+__device__ __forceinline__ void transpose_lines(uint64_t* lines) {
   uint32_t lo[8], hi[8];
 #pragma unroll
   for (int y = 0; y < 8; ++y) {
-    const uint64_t r = y < H ? rows[y * TILE] : 0ull;
+    const uint64_t r = lines[y * TILE];
     lo[y] = (uint32_t)r;
     hi[y] = (uint32_t)(r >> 32);
   }
@@ -84,10 +88,8 @@ __device__ __forceinline__ void build_cols(const uint64_t* rows, uint64_t* cols)
   transpose4x4(hi[0], hi[1], hi[2], hi[3], c[0], c[1], c[2], c[3]);  // x 4..7, y 0..3
   transpose4x4(hi[4], hi[5], hi[6], hi[7], d[0], d[1], d[2], d[3]);  // x 4..7, y 4..7
 #pragma unroll
-  for (int x = 0; x < W; ++x) {
-    const uint64_t v = x < 4 ? ((uint64_t)b[x] << 32) | a[x] : ((uint64_t)d[x - 4] << 32) | c[x - 4];
-    cols[x * TILE] = v;
-  }
+  for (int x = 0; x < 8; ++x)
+    lines[x * TILE] = x < 4 ? ((uint64_t)b[x] << 32) | a[x] : ((uint64_t)d[x - 4] << 32) | c[x - 4];
 }
 
 __device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) {
@@ -98,7 +100,7 @@ __device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) 
   return __double2float_rn(__dsub_rn(1.0, p));
 }
 
-// ------------------------------------------------------------------ kernel
+// ------------------------------------------------------------------ tile body
 // Lane <-> env mapping inside a tile: thread tid = 32*w + l (warp w, lane l)
 // owns tile-local env le = 4*l + w.  All state arrays are indexed by the
 // "slot" tid, so every warp access to them is contiguous; caller arrays
@@ -107,60 +109,67 @@ __device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) 
 // misalignment M = 147*le mod 4 = 3w mod 4 and the record emission is
 // specialised per warp at compile time (no per-lane shifts, and the
 // per-lane SMEM word stride 147 is odd: bank-conflict free).
-template <int FAM, int H, int W, int MODE>
-__global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
-  using C = Cfg<FAM, H, W>;
-  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
-  __shared__ __align__(16) uint64_t s_rows[8][TILE];
-  __shared__ __align__(16) uint64_t s_cols[8][TILE];
-  __shared__ __align__(16) uint64_t s_agent[TILE];
-  __shared__ __align__(16) uint32_t s_balls[FAM == FAM_DYNOBS ? TILE : 4];
-  __shared__ __align__(16) uint32_t s_episode[FAM == FAM_DYNOBS ? TILE : 4];
-  __shared__ __align__(16) uint8_t s_act[TILE];
-  __shared__ __align__(8) uint64_t s_mbar;
 
+// One tile's input buffers in SMEM (filled by TMA bulk copies).
+template <int FAM>
+struct TileSmem {
+  uint64_t rows[8][TILE];                            // grid rows; later this env's view lines
+  uint64_t agent[TILE];                              // agent records
+  uint32_t balls[FAM == FAM_DYNOBS ? TILE : 4];      // DynObs ball positions
+  uint32_t episode[FAM == FAM_DYNOBS ? TILE : 4];    // DynObs episode counters
+  uint8_t act[TILE];                                 // actions (env order)
+};
+
+// Thread 0: bulk-copy tile `tile`'s inputs into `b`, completing on `mbar`.
+// Returns whether the actions came along (full tile, 16-B aligned base).
+template <int FAM, int H, int MODE>
+__device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint32_t mbar) {
+  const int64_t tile0 = tile * TILE;
+  const bool act_bulk = MODE == MODE_STEP && a.bulk_act && tile0 + TILE <= a.n;
+  const uint32_t bytes = H * TILE * 8 + TILE * 8 + (act_bulk ? TILE : 0) +
+                         (FAM == FAM_DYNOBS ? (MODE == MODE_STEP ? 8 : 4) * TILE : 0);
+  mbar_expect_tx(mbar, bytes);
+  bulk_g2s(&b.rows[0][0], a.grid + tile0 * H, H * TILE * 8, mbar);
+  bulk_g2s(b.agent, a.agent + tile0, TILE * 8, mbar);
+  if (act_bulk) bulk_g2s(b.act, a.actions + tile0, TILE, mbar);
+  if (FAM == FAM_DYNOBS) {
+    bulk_g2s(b.balls, a.balls + tile0, TILE * 4, mbar);
+    if (MODE == MODE_STEP) bulk_g2s(b.episode, a.episode + tile0, TILE * 4, mbar);
+  }
+  return act_bulk;
+}
+
+// Everything a tile does once its inputs are in SMEM (MODE != RESET) or
+// without inputs (RESET): a2-a7 for this thread's env, the obs bulk store
+// issued by thread 0 (the caller waits for it before reusing s_obs).
+// The caller guarantees s_obs is free (the previous bulk store has read it).
+template <int FAM, int H, int W, int MODE>
+__device__ __forceinline__ void tile_body(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint8_t* s_obs) {
+  using C = Cfg<FAM, H, W>;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int le = 4 * lane + warp;
-  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  const int64_t tile0 = tile * TILE;
   const int64_t slot = tile0 + tid;   // state index
   const int64_t e = tile0 + le;       // env index (caller arrays)
   const bool valid = e < a.n;
   const uint32_t genv = a.env_begin + (uint32_t)e;  // global env index: Philox counter word c0
-  uint64_t* const rows = &s_rows[0][tid];
-  uint64_t* const cols = &s_cols[0][tid];
+  uint64_t* const rows = &b.rows[0][tid];
   RowView g{rows};
 
-  // ---- a1: stage: one TMA bulk copy per array brings the tile's grid rows,
-  // agent records and actions (and DynObs balls / episode counters) into SMEM
+  // ---- a1: decode the staged inputs
   uint8_t act = 0;
   uint64_t rec = 0;
   uint32_t balls = 0, episode = 0;
   if (MODE != MODE_RESET) {
-    const bool full = tile0 + TILE <= a.n;
-    const bool act_bulk = MODE == MODE_STEP && a.bulk_act && full;
-    const uint32_t mbar = smem_u32(&s_mbar);
-    if (tid == 0) {
-      mbar_init(mbar, 1);
-      const uint32_t bytes = H * TILE * 8 + TILE * 8 + (act_bulk ? TILE : 0) +
-                             (FAM == FAM_DYNOBS ? (MODE == MODE_STEP ? 8 : 4) * TILE : 0);
-      mbar_expect_tx(mbar, bytes);
-      bulk_g2s(&s_rows[0][0], a.grid + tile0 * H, H * TILE * 8, mbar);
-      bulk_g2s(s_agent, a.agent + tile0, TILE * 8, mbar);
-      if (act_bulk) bulk_g2s(s_act, a.actions + tile0, TILE, mbar);
-      if (FAM == FAM_DYNOBS) {
-        bulk_g2s(s_balls, a.balls + tile0, TILE * 4, mbar);
-        if (MODE == MODE_STEP) bulk_g2s(s_episode, a.episode + tile0, TILE * 4, mbar);
-      }
+    rec = b.agent[tid];
+    if (MODE == MODE_STEP && valid) {
+      const bool act_bulk = a.bulk_act && tile0 + TILE <= a.n;
+      act = act_bulk ? b.act[le] : a.actions[e];
     }
-    if (MODE == MODE_STEP && !act_bulk && valid) act = a.actions[e];
-    __syncthreads();  // mbarrier initialised before anyone waits on it
-    mbar_wait(mbar, 0);
-    rec = s_agent[tid];
-    if (act_bulk) act = s_act[le];
     if (FAM == FAM_DYNOBS) {
-      balls = s_balls[tid];
-      if (MODE == MODE_STEP) episode = s_episode[tid];
+      balls = b.balls[tid];
+      if (MODE == MODE_STEP) episode = b.episode[tid];
     }
   }
   int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
@@ -191,8 +200,8 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
   } else {
     if (FAM == FAM_DYNOBS) {
 #pragma unroll
-      for (int b = 0; b < C::NOBST; ++b) {
-        const uint32_t p = (balls >> (8 * b)) & 0xFF;
+      for (int bb = 0; bb < C::NOBST; ++bb) {
+        const uint32_t p = (balls >> (8 * bb)) & 0xFF;
         if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
       }
     }
@@ -208,8 +217,8 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
         not_clear = f0 != CELL_EMPTY && (f0 & 15) != K_GOAL;
         const uint4 u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
 #pragma unroll
-        for (int b = 0; b < C::NOBST; ++b) {
-          const uint32_t p = (balls >> (8 * b)) & 0xFF;
+        for (int bb = 0; bb < C::NOBST; ++bb) {
+          const uint32_t p = (balls >> (8 * bb)) & 0xFF;
           if (!p) continue;
           const int bx = p >> 4, by = p & 15;
           uint32_t m = 0;
@@ -220,12 +229,12 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
             m |= (ok ? 1u : 0u) << k;
           }
           if (m) {
-            const uint32_t ub = b == 0 ? u.x : b == 1 ? u.y : b == 2 ? u.z : u.w;
+            const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
             const int k = select64(m, bounded(ub, __popc(m)));
             const int nx = bx - 1 + k % 3, ny = by - 1 + k / 3;
             g.set(nx, ny, make_cell(K_BALL, COL_BLUE));
             g.set(bx, by, CELL_EMPTY);
-            balls = (balls & ~(0xFFu << (8 * b))) | ((uint32_t)((nx << 4) | ny) << (8 * b));
+            balls = (balls & ~(0xFFu << (8 * bb))) | ((uint32_t)((nx << 4) | ny) << (8 * bb));
           }
         }
       }
@@ -280,13 +289,20 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
     }
   }
 
-  // ---- a6: observation (obs.cuh)
-  build_cols<H, W>(rows, cols);
+  // ---- a7a: grid write-back (only when modified), before the lines are reused
+  if (MODE != MODE_OBSERVE && grid_dirty) {
+    uint64_t* gdst = a.grid + tile0 * H + tid;
+#pragma unroll
+    for (int y = 0; y < H; ++y)
+      gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : rows[y * TILE];
+  }
+
+  // ---- a6: observation (obs.cuh); odd directions read world columns
+  if (dir & 1) transpose_lines(rows);
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
-    const int rec_byte = le * OBS_BYTES;
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
-    observe_emit(rows, cols, ax, ay, dir, carry, s32 + ((rec_byte - M) >> 2), M);
+    observe_emit(rows, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
 
   // ---- a7: stores
@@ -294,8 +310,7 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
   const int nvalid = nvalid64 >= TILE ? TILE : (int)nvalid64;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  const bool bulk = a.bulk_obs && nvalid == TILE;
-  if (bulk) {
+  if (a.bulk_obs && nvalid == TILE) {
     if (tid == 0) {
       uint8_t* dst = a.obs + tile0 * OBS_BYTES;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-  } else {
+  } else {  // partial tile / unaligned obs: plain stores
     uint8_t* dst = a.obs + tile0 * OBS_BYTES;
     for (int i = tid; i < nvalid * OBS_BYTES; i += TILE) dst[i] = s_obs[i];
   }
@@ -321,31 +336,90 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
       if (regen) a.episode[slot] = episode;
       if (FAM == FAM_DYNOBS) a.balls[slot] = balls;
     }
-    if (grid_dirty) {
-      uint64_t* gdst = a.grid + tile0 * H + tid;
-#pragma unroll
-      for (int y = 0; y < H; ++y)
-        gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : rows[y * TILE];
-    }
     // episode statistics (info i_{t+1}): warp reduce -> striped atomics
-    {
-      const unsigned any = __any_sync(0xffffffffu, (st_ep | st_fail) != 0 && valid);
-      if (any) {
-        const uint32_t vv = valid ? 1u : 0u;
-        uint32_t v[8] = {st_ep * vv, st_len * vv, st_succ * vv, st_succ_len * vv,
-                         st_lava * vv, st_coll * vv, st_trunc * vv, st_fail * vv};
+    const unsigned any = __any_sync(0xffffffffu, (st_ep | st_fail) != 0 && valid);
+    if (any) {
+      const uint32_t vv = valid ? 1u : 0u;
+      uint32_t v[8] = {st_ep * vv, st_len * vv, st_succ * vv, st_succ_len * vv,
+                       st_lava * vv, st_coll * vv, st_trunc * vv, st_fail * vv};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
-        if (lane == 0) {
-          unsigned long long* st = a.stats + (size_t)((blockIdx.x * (TILE / 32) + warp) % NSLOT) * 8;
+      for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
+      if (lane == 0) {
+        unsigned long long* st = a.stats + (size_t)((tile * (TILE / 32) + warp) % NSLOT) * 8;
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (v[k]) atomicAdd(st + k, (unsigned long long)v[k]);
-        }
+        for (int k = 0; k < 8; ++k)
+          if (v[k]) atomicAdd(st + k, (unsigned long long)v[k]);
       }
     }
   }
-  if (bulk && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ kernels
+// One tile per CTA (reset, observe, and steps of small batches).
+template <int FAM, int H, int W, int MODE>
+__global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
+  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
+  __shared__ __align__(128) TileSmem<FAM> s_buf;
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (MODE != MODE_RESET) {
+    const uint32_t mbar = smem_u32(&s_mbar);
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      issue_tile_loads<FAM, H, MODE>(a, blockIdx.x, s_buf, mbar);
+    }
+    __syncthreads();  // mbarrier initialised before anyone waits on it
+    mbar_wait(mbar, 0);
+  }
+  tile_body<FAM, H, W, MODE>(a, blockIdx.x, s_buf, s_obs);
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Persistent step: each CTA pulls tiles from a global atomic scheduler and
+// prefetches the next tile's inputs (TMA, double-buffered, mbarrier-tracked)
+// while it computes the current one.  The last CTA to finish resets the
+// scheduler, so the kernel can be replayed from a CUDA graph.
+template <int FAM, int H, int W>
+__global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
+  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
+  __shared__ __align__(128) TileSmem<FAM> s_buf[2];
+  __shared__ __align__(8) uint64_t s_mbar[2];
+  __shared__ int64_t s_tile[2];
+  const int64_t n_tiles = (a.n + TILE - 1) / TILE;
+  unsigned int* const sched = a.sched;  // [0] next tile, [1] CTAs done
+  const int tid = threadIdx.x;
+  // thread 0: fetch the next tile index, publish it in s_tile[k] and start its
+  // loads on s_mbar[k]; with no tile left it only arrives (phase completes), so
+  // waiting on s_mbar[k] always makes s_tile[k] visible.
+  auto fetch = [&](int k) {
+    const int64_t t = atomicAdd(&sched[0], 1u);
+    s_tile[k] = t;
+    if (t < n_tiles) issue_tile_loads<FAM, H, MODE_STEP>(a, t, s_buf[k], smem_u32(&s_mbar[k]));
+    else mbar_arrive(smem_u32(&s_mbar[k]));
+  };
+  if (tid == 0) {
+    mbar_init(smem_u32(&s_mbar[0]), 1);
+    mbar_init(smem_u32(&s_mbar[1]), 1);
+    fetch(0);
+  }
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int cur = it & 1;
+    mbar_wait(smem_u32(&s_mbar[cur]), (uint32_t)(it >> 1) & 1u);
+    const int64_t tile = s_tile[cur];
+    if (tile >= n_tiles) break;
+    if (tid == 0) fetch(cur ^ 1);  // buffer cur^1 was released by the barrier ending the last tile
+    tile_body<FAM, H, W, MODE_STEP>(a, tile, s_buf[cur], s_obs);
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();  // s_obs and s_buf[cur] free for reuse
+  }
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __threadfence();
+    if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the scheduler
+      atomicExch(&sched[0], 0u);
+      atomicExch(&sched[1], 0u);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ other kernels
@@ -376,10 +450,25 @@ __global__ void stats_reduce_kernel(const unsigned long long* slots, long long* 
 // ------------------------------------------------------------------ dispatch
 template <int FAM, int H, int W>
 static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
-  const dim3 grid((unsigned)n_tiles), block(TILE);
-  if (mode == MODE_STEP) navix_kernel<FAM, H, W, MODE_STEP><<<grid, block, 0, s>>>(a);
-  else if (mode == MODE_RESET) navix_kernel<FAM, H, W, MODE_RESET><<<grid, block, 0, s>>>(a);
-  else navix_kernel<FAM, H, W, MODE_OBSERVE><<<grid, block, 0, s>>>(a);
+  const dim3 block(TILE);
+  if (mode == MODE_STEP) {
+    // persistent grid: as many CTAs as fit on the device at once
+    static int per_sm = -1, n_sm = -1;
+    if (per_sm < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W>, TILE, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t cap = (int64_t)per_sm * n_sm;
+    const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
+    navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
+  } else if (mode == MODE_RESET) {
+    navix_kernel<FAM, H, W, MODE_RESET><<<(unsigned)n_tiles, block, 0, s>>>(a);
+  } else {
+    navix_kernel<FAM, H, W, MODE_OBSERVE><<<(unsigned)n_tiles, block, 0, s>>>(a);
+  }
   return cudaPeekAtLastError();
 }
 
