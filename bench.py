@@ -90,6 +90,34 @@ class ClockSampler:
                 pass
             time.sleep(self.period)
 
+    def sample_once(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for k, bit in names.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def poll_until(self, event):
+        """Sample until `event` (recorded at the end of the timed region) completes."""
+        if not self.ok:
+            return
+        while True:
+            done = event.query()
+            try:
+                self.sample_once()
+            except Exception:
+                return
+            if done:
+                return
+
     def __enter__(self):
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
@@ -180,17 +208,19 @@ def run_navix(args, rank, world, local_rank):
     import numpy as np
     import torch
 
-    from paper_2407_19396_b200 import NavixEnv, shard_range
+    from paper_2407_19396_b200 import NavixEnv
+    from paper_2407_19396_b200.distributed import (all_reduce_stats, init_process_group, max_over_ranks,
+                                                   mean_legacy_return, shard_for)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_process_group("nccl", dev)
     n_total = args.envs_per_gpu * world
-    begin, end = shard_range(n_total, rank, world)
-    n = end - begin
+    sh = shard_for(n_total, rank, world)
+    begin, end, n = sh.begin, sh.end, sh.n
     env = NavixEnv(args.env, n, seed=0, env_begin=begin, num_envs_total=n_total, device=dev)
     spec = env.spec
     B = algorithmic_bytes(spec)
@@ -227,30 +257,26 @@ def run_navix(args, rank, world, local_rank):
     barrier()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        ev0.record(s)
-        if graphs:
-            for gph in graphs:
-                gph.replay()
-        else:
-            for t in range(args.steps):
-                env.step(acts[t % ring])
-        ev1.record(s)
-        torch.cuda.synchronize(dev)
+    clk = ClockSampler(local_rank)
+    barrier()
+    ev0.record(s)
+    if graphs:
+        for gph in graphs:
+            gph.replay()
+    else:
+        for t in range(args.steps):
+            env.step(acts[t % ring])
+    ev1.record(s)
+    # the launches are queued: sample clocks / throttle reasons from the host
+    # while the device is still inside the timed region
+    clk.poll_until(ev1)
+    torch.cuda.synchronize(dev)
     t_local = ev0.elapsed_time(ev1) / 1e3
-    t_max = t_local
-    if dist is not None:
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(t_local, dev)
     value = n_total * args.steps / t_max
 
     # episode statistics: the one collective of the path (NCCL all-reduce of int64[8])
-    st = env.stats().clone()
-    if dist is not None:
-        dist.all_reduce(st)
-    st = st.cpu().numpy()
+    st = all_reduce_stats(env.stats()).cpu().numpy()
 
     # end to end through the host-buffer C-ABI call (H2D actions, D2H outputs)
     h_act = torch.from_numpy(np.ascontiguousarray(acts[: args.e2e_steps].cpu().numpy())).pin_memory()
@@ -263,11 +289,7 @@ def run_navix(args, rank, world, local_rank):
     t0 = time.perf_counter()
     for t in range(args.e2e_steps):
         env.step_host(h_act[t], h_obs, h_rew, h_te, h_tr)
-    t_e2e = time.perf_counter() - t0
-    if dist is not None:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
+    t_e2e = max_over_ranks(time.perf_counter() - t0, dev)
     e2e_value = n_total * args.e2e_steps / t_e2e
 
     if rank != 0:
@@ -307,6 +329,7 @@ def run_navix(args, rank, world, local_rank):
         "episode_stats": {k: int(v) for k, v in zip(
             ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_collision", "n_truncated",
              "gen_failures"), st)},
+        "mean_episode_return_minigrid": mean_legacy_return(st, spec.max_steps),
         "host": {"cpu_model": model, "nproc": ncpu},
     }
     print(json.dumps(line), flush=True)

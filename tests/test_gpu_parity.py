@@ -179,3 +179,28 @@ def test_unaligned_obs_buffer_uses_plain_stores():
         a.step(acts[t], out=out)
         ro = b.step(acts[t])[0]
         assert torch.equal(view, ro)
+
+
+def test_cuda_graph_replay_matches_eager():
+    """The bench times CUDA-graph replays of the persistent step kernel (its
+    tile scheduler resets itself at the end of every launch)."""
+    NavixEnv = navix()
+    n, K = 5000, 40
+    a = NavixEnv("DoorKey-8x8-v0", n, seed=3)
+    b = NavixEnv("DoorKey-8x8-v0", n, seed=3)
+    a.reset()
+    b.reset()
+    acts = a.sample_actions(1, 0, K)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for t in range(K):
+            a.step(acts[t])
+    for rep in range(3):  # capture does not execute; replay 3 times = 3*K steps
+        graph.replay()
+        for t in range(K):
+            b.step(acts[t])
+        torch.cuda.synchronize()
+        assert np.array_equal(a.export_state(), b.export_state()), rep
+    assert torch.equal(a.obs, b.obs) and torch.equal(a.reward, b.reward)
+    assert torch.equal(a.stats(), b.stats())
