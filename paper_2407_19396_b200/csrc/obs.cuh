@@ -29,17 +29,18 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return d;
 }
 
-// SWAR encode of 4 cell bytes (invisible cells already zeroed) to MiniGrid
-// (type, colour, state): kind >= 11 (closed 11 / locked 12 door) -> type 4,
-// state kind-10; otherwise type = kind, state 0; colour = bits 4-6.
-__device__ __forceinline__ void encode4(uint32_t w, uint32_t& ty, uint32_t& co, uint32_t& st) {
-  const uint32_t E = w & 0x0F0F0F0Fu;
-  co = (w >> 4) & 0x07070707u;
-  const uint32_t ge = (E + 0x05050505u) & 0x10101010u;
-  const uint32_t d = ge >> 4;
-  const uint32_t dm = ge - d;
-  ty = (E & ~dm) | (d << 2);
-  st = (E & dm) - d * 10u;
+// SWAR encode of 4 cell bytes w with visibility byte mask m (0xFF visible,
+// 0x00 invisible -> (0,0,0)) to MiniGrid (type, colour, state):
+// kind >= 11 (closed 11 / locked 12 door) -> type 4, state kind-10; otherwise
+// type = kind, state 0; colour = bits 4-6.  E + 0x75 sets bit 7 of a byte iff
+// kind >= 11, and a sign-replicating byte permute turns it into a 0xFF mask.
+__device__ __forceinline__ void encode4(uint32_t w, uint32_t m, uint32_t& ty, uint32_t& co, uint32_t& st) {
+  const uint32_t E = w & m & 0x0F0F0F0Fu;
+  co = (w >> 4) & m & 0x07070707u;
+  uint32_t D;
+  asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(D) : "r"(E + 0x75757575u));
+  ty = (E & ~D) | (D & 0x04040404u);
+  st = (E + 0x06060606u) & D & 0x0F0F0F0Fu;  // (kind + 16 - 10) mod 16, no borrow between bytes
 }
 
 // ---------------------------------------------------------------- emission plan
@@ -172,11 +173,11 @@ __device__ __forceinline__ void emit_record(uint32_t* out, uint32_t (&r)[7][7]) 
 __device__ __forceinline__ void encode_col(uint32_t c_lo, uint32_t c_hi, uint32_t m_lo, uint32_t m_hi, uint32_t pend,
                                            uint32_t (&r)[7]) {
   uint32_t ty, co, st;
-  encode4(c_lo & m_lo, ty, co, st);
+  encode4(c_lo, m_lo, ty, co, st);
   r[0] = prmt(ty, co, 0x5140);  // t0 c0 t1 c1
   r[1] = prmt(ty, co, 0x7362);  // t2 c2 t3 c3
   r[2] = st;
-  encode4(c_hi & m_hi, ty, co, st);
+  encode4(c_hi, m_hi, ty, co, st);
   r[3] = prmt(ty, co, 0x5140);
   r[4] = prmt(ty, co, 0x7362);
   r[5] = st;
@@ -224,19 +225,19 @@ __device__ __forceinline__ void observe_emit(const uint64_t* lines, int ax, int 
   // one carry chain on X = S | rev(S) << 8 over T2 = T | rev(T) << 8 (bit 7 = 0
   // stops the carry between the halves)
   uint32_t vis_lo = 0, vis_hi = 0;
-  uint32_t seed = 1u << 3;
+  uint32_t seed = 1u << 3;  // bits 0-6 (bit 7 may hold garbage: the carry stopper absorbs it)
 #pragma unroll
   for (int j = 6; j >= 0; --j) {
     const uint32_t tw = j < 4 ? t_lo : t_hi, trw = j < 4 ? tr_lo : tr_hi;
     const uint32_t b = (uint32_t)(j & 3);
-    const uint32_t t2 = prmt(tw, trw, 0x4400u | ((4u + b) << 4) | b) & 0x7F7Fu;  // byte0 = t, byte1 = rev t
-    const uint32_t t = t2 & 0x7Fu;
-    const uint32_t x = seed | ((__brev(seed) >> 25) << 8);
+    // t2 = T | rev(T) << 8 (bits 7 and 15 zero: carry stoppers)
+    const uint32_t t2 = prmt(tw, trw, 0x4400u | ((4u + b) << 4) | b) & 0x7F7Fu;
+    const uint32_t x = seed | (__brev(seed) >> 17);   // S | rev(S) << 8
     const uint32_t tx = t2 & x;
-    const uint32_t v2 = x | ((t2 + tx) ^ t2 ^ tx);
-    const uint32_t v = (v2 | (__brev(v2 >> 8) >> 25)) & 0x7Fu;
-    const uint32_t av = v & t;
-    seed = (av | (av << 1) | (av >> 1)) & 0x7Fu;
+    const uint32_t v2 = x | ((t2 + tx) ^ (t2 ^ tx));  // R(S) | rev(L(S)) << 8 (carry chains)
+    const uint32_t v = (v2 | (__brev(v2) >> 17)) & 0x7Fu;
+    const uint32_t av = v & t2;
+    seed = av | (av << 1) | (av >> 1);
     if (j < 4) vis_lo |= v << (8 * j);
     else vis_hi |= v << (8 * (j - 4));
   }
@@ -245,8 +246,8 @@ __device__ __forceinline__ void observe_emit(const uint64_t* lines, int ax, int 
   uint32_t r[7][7];
 #pragma unroll
   for (int vi = 0; vi < 7; ++vi) {
-    const uint32_t m_lo = prmt(vis_lo << (7 - vi), 0u, 0xBA98u);
-    const uint32_t m_hi = prmt(vis_hi << (7 - vi), 0u, 0xBA98u);
+    const uint32_t m_lo = prmt(vis_lo * (1u << (7 - vi)), 0u, 0xBA98u);  // multiply: FMA pipe
+    const uint32_t m_hi = prmt(vis_hi * (1u << (7 - vi)), 0u, 0xBA98u);
     encode_col(clo[vi], chi[vi], m_lo, m_hi, 0u, r[vi]);
   }
   switch (M) {  // one warp-uniform dispatch for the whole record

@@ -22,6 +22,7 @@
 //                 grid rows written back only when modified; episode
 //                 statistics warp-reduced into striped int64 counters.
 #include <cstdint>
+#include <cstdlib>
 
 #include "layout.h"
 #include "levelgen.cuh"
@@ -46,7 +47,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred P1;\nLAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n"
       "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}" ::"r"(mbar),
       "r"(parity)
       : "memory");
@@ -142,9 +143,20 @@ __device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t ti
 // Everything a tile does once its inputs are in SMEM (MODE != RESET) or
 // without inputs (RESET): a2-a7 for this thread's env, the obs bulk store
 // issued by thread 0 (the caller waits for it before reusing s_obs).
-// The caller guarantees s_obs is free (the previous bulk store has read it).
-template <int FAM, int H, int W, int MODE>
-__device__ __forceinline__ void tile_body(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint8_t* s_obs) {
+// Per-thread results of a tile, written out by tile_store().
+struct EnvResult {
+  float reward;
+  bool valid, regen, term, trunc;
+  uint64_t nrec;
+  uint32_t episode, balls;
+  uint32_t st[8];
+};
+
+// a1-a6 for this thread's env: compute, then write its obs record into s_obs
+// (after before_emit() has made sure s_obs is free).
+template <int FAM, int H, int W, int MODE, class BeforeEmit>
+__device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint8_t* s_obs,
+                                                  BeforeEmit before_emit) {
   using C = Cfg<FAM, H, W>;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -299,65 +311,85 @@ __device__ __forceinline__ void tile_body(const KernelArgs& a, int64_t tile, Til
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
   if (dir & 1) transpose_lines(rows);
+  before_emit();
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
     observe_emit(rows, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
 
-  // ---- a7: stores
-  const int64_t nvalid64 = a.n - tile0;
-  const int nvalid = nvalid64 >= TILE ? TILE : (int)nvalid64;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
+  EnvResult r;
+  r.reward = reward;
+  r.valid = valid;
+  r.regen = regen;
+  r.term = term;
+  r.trunc = trunc;
+  r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
+           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48);
+  r.episode = episode;
+  r.balls = balls;
+  const uint32_t vv = valid ? 1u : 0u;
+  r.st[0] = st_ep * vv; r.st[1] = st_len * vv; r.st[2] = st_succ * vv; r.st[3] = st_succ_len * vv;
+  r.st[4] = st_lava * vv; r.st[5] = st_coll * vv; r.st[6] = st_trunc * vv; r.st[7] = st_fail * vv;
+  return r;
+}
+
+// a7: the tile's obs leave SMEM in one TMA bulk store (full tile, 16-B aligned
+// destination) issued by one thread, else with plain stores by `nthr` threads.
+__device__ __forceinline__ void store_obs(const KernelArgs& a, int64_t tile, const uint8_t* s_obs, int t, int nthr,
+                                          bool issuer) {
+  const int64_t tile0 = tile * TILE;
+  const int64_t nv = a.n - tile0;
+  const int nvalid = nv >= TILE ? TILE : (int)nv;
+  uint8_t* dst = a.obs + tile0 * OBS_BYTES;
   if (a.bulk_obs && nvalid == TILE) {
-    if (tid == 0) {
-      uint8_t* dst = a.obs + tile0 * OBS_BYTES;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                   "r"(smem_u32(s_obs)), "r"((uint32_t)(TILE * OBS_BYTES))
+    if (issuer) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(s_obs)),
+                   "r"((uint32_t)(TILE * OBS_BYTES))
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-  } else {  // partial tile / unaligned obs: plain stores
-    uint8_t* dst = a.obs + tile0 * OBS_BYTES;
-    for (int i = tid; i < nvalid * OBS_BYTES; i += TILE) dst[i] = s_obs[i];
+  } else {
+    for (int i = t; i < nvalid * OBS_BYTES; i += nthr) dst[i] = s_obs[i];
   }
+}
 
-  if (MODE != MODE_OBSERVE) {
-    if (valid) {
-      if (MODE == MODE_STEP) {
-        a.reward[e] = reward;
-        a.terminated[e] = term;
-        a.truncated[e] = trunc;
-      }
-      const uint64_t nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) |
-                            ((uint64_t)carry << 24) | ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48);
-      a.agent[slot] = nrec;
-      if (regen) a.episode[slot] = episode;
-      if (FAM == FAM_DYNOBS) a.balls[slot] = balls;
+// a7: per-env global stores and the episode statistics.
+template <int FAM, int MODE>
+__device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, const EnvResult& r) {
+  if (MODE == MODE_OBSERVE) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t slot = tile * TILE + tid, e = tile * TILE + 4 * lane + warp;
+  if (r.valid) {
+    if (MODE == MODE_STEP) {
+      a.reward[e] = r.reward;
+      a.terminated[e] = r.term;
+      a.truncated[e] = r.trunc;
     }
-    // episode statistics (info i_{t+1}): warp reduce -> striped atomics
-    const unsigned any = __any_sync(0xffffffffu, (st_ep | st_fail) != 0 && valid);
-    if (any) {
-      const uint32_t vv = valid ? 1u : 0u;
-      uint32_t v[8] = {st_ep * vv, st_len * vv, st_succ * vv, st_succ_len * vv,
-                       st_lava * vv, st_coll * vv, st_trunc * vv, st_fail * vv};
+    a.agent[slot] = r.nrec;
+    if (r.regen) a.episode[slot] = r.episode;
+    if (FAM == FAM_DYNOBS) a.balls[slot] = r.balls;
+  }
+  // episode statistics (info i_{t+1}): warp reduce -> striped atomics
+  const unsigned any = __any_sync(0xffffffffu, (r.st[0] | r.st[7]) != 0);
+  if (any) {
+    uint32_t v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
-      if (lane == 0) {
-        unsigned long long* st = a.stats + (size_t)((tile * (TILE / 32) + warp) % NSLOT) * 8;
+    for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(0xffffffffu, r.st[k]);
+    if (lane == 0) {
+      unsigned long long* st = a.stats + (size_t)((tile * (TILE / 32) + warp) % NSLOT) * 8;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (v[k]) atomicAdd(st + k, (unsigned long long)v[k]);
-      }
+      for (int k = 0; k < 8; ++k)
+        if (v[k]) atomicAdd(st + k, (unsigned long long)v[k]);
     }
   }
 }
 
 // ------------------------------------------------------------------ kernels
-// One tile per CTA (reset, observe, and steps of small batches).
+// One tile per CTA (reset, observe; step when NAVIX_STEP_KERNEL=onetile).
+// 28 KB of SMEM: up to 8 CTAs per SM with <= 64 registers.
 template <int FAM, int H, int W, int MODE>
-__global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(TILE, 8) navix_kernel(const KernelArgs a) {
   __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
   __shared__ __align__(128) TileSmem<FAM> s_buf;
   __shared__ __align__(8) uint64_t s_mbar;
@@ -370,28 +402,37 @@ __global__ void __launch_bounds__(TILE) navix_kernel(const KernelArgs a) {
     __syncthreads();  // mbarrier initialised before anyone waits on it
     mbar_wait(mbar, 0);
   }
-  tile_body<FAM, H, W, MODE>(a, blockIdx.x, s_buf, s_obs);
+  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, s_buf, s_obs, [] {});
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  store_obs(a, blockIdx.x, s_obs, threadIdx.x, TILE, threadIdx.x == 0);
+  tile_store<FAM, MODE>(a, blockIdx.x, r);
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Persistent step: each CTA pulls tiles from a global atomic scheduler and
-// prefetches the next tile's inputs (TMA, double-buffered, mbarrier-tracked)
-// while it computes the current one.  The last CTA to finish resets the
-// scheduler, so the kernel can be replayed from a CUDA graph.
+// keeps the next tile's inputs in flight (TMA, double-buffered, mbarrier-
+// tracked) while it computes the current one.  Per tile: one CTA barrier after
+// the obs emission (thread 0 then issues the tile's TMA store and the
+// prefetch of the tile-after-next into the released input buffer) and one
+// before the next tile's emission, by which time the store has long read the
+// staging buffer.  The scheduler atomic is issued a whole tile early.  (A barrier-free
+// variant where the last warp to finish issues the store measured 1.3 % slower:
+// its warps spin on mbarriers instead.)  The last CTA to finish resets the
+// scheduler, so the kernel replays from a CUDA graph.
 template <int FAM, int H, int W>
 __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
   __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
   __shared__ __align__(128) TileSmem<FAM> s_buf[2];
-  __shared__ __align__(8) uint64_t s_mbar[2];
+  __shared__ __align__(8) uint64_t s_mbar[2];   // tile inputs landed (per buffer)
   __shared__ int64_t s_tile[2];
   const int64_t n_tiles = (a.n + TILE - 1) / TILE;
-  unsigned int* const sched = a.sched;  // [0] next tile, [1] CTAs done
+  unsigned int* const sched = a.sched;          // [0] next tile, [1] CTAs done
   const int tid = threadIdx.x;
-  // thread 0: fetch the next tile index, publish it in s_tile[k] and start its
-  // loads on s_mbar[k]; with no tile left it only arrives (phase completes), so
-  // waiting on s_mbar[k] always makes s_tile[k] visible.
-  auto fetch = [&](int k) {
-    const int64_t t = atomicAdd(&sched[0], 1u);
+  // fetch the next tile index into s_tile[k] and start its loads on s_mbar[k];
+  // with no tile left only arrive (the phase completes), so waiting on
+  // s_mbar[k] always publishes s_tile[k].
+  auto publish = [&](int k, int64_t t) {
     s_tile[k] = t;
     if (t < n_tiles) issue_tile_loads<FAM, H, MODE_STEP>(a, t, s_buf[k], smem_u32(&s_mbar[k]));
     else mbar_arrive(smem_u32(&s_mbar[k]));
@@ -399,7 +440,8 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   if (tid == 0) {
     mbar_init(smem_u32(&s_mbar[0]), 1);
     mbar_init(smem_u32(&s_mbar[1]), 1);
-    fetch(0);
+    publish(0, atomicAdd(&sched[0], 1u));
+    publish(1, atomicAdd(&sched[0], 1u));
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -407,10 +449,20 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     mbar_wait(smem_u32(&s_mbar[cur]), (uint32_t)(it >> 1) & 1u);
     const int64_t tile = s_tile[cur];
     if (tile >= n_tiles) break;
-    if (tid == 0) fetch(cur ^ 1);  // buffer cur^1 was released by the barrier ending the last tile
-    tile_body<FAM, H, W, MODE_STEP>(a, tile, s_buf[cur], s_obs);
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();  // s_obs and s_buf[cur] free for reuse
+    // claim the tile-after-next now: the atomic's latency hides behind the compute
+    unsigned int next = 0;
+    if (tid == 0) next = atomicAdd(&sched[0], 1u);
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(a, tile, s_buf[cur], s_obs, [&] {
+      if (it > 0) {  // the previous tile's store must have read s_obs
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+      }
+    });
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();  // all records in s_obs; input buffer cur no longer read
+    store_obs(a, tile, s_obs, tid, TILE, tid == 0);
+    if (tid == 0) publish(cur, next);  // tile-after-next into the released buffer
+    tile_store<FAM, MODE_STEP>(a, tile, r);
   }
   if (tid == 0) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -451,7 +503,14 @@ __global__ void stats_reduce_kernel(const unsigned long long* slots, long long* 
 template <int FAM, int H, int W>
 static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
   const dim3 block(TILE);
-  if (mode == MODE_STEP) {
+  static int onetile = -1;
+  if (onetile < 0) {
+    const char* v = getenv("NAVIX_STEP_KERNEL");  // experiment switch
+    onetile = v && v[0] == 'o';
+  }
+  if (mode == MODE_STEP && onetile) {
+    navix_kernel<FAM, H, W, MODE_STEP><<<(unsigned)n_tiles, block, 0, s>>>(a);
+  } else if (mode == MODE_STEP) {
     // persistent grid: as many CTAs as fit on the device at once
     static int per_sm = -1, n_sm = -1;
     if (per_sm < 0) {
