@@ -125,29 +125,28 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
   } else if constexpr (FAM == FAM_KEYCORRIDOR) {
     // [MG] RoomGrid._gen_grid + KeyCorridorEnv._gen_grid + connect_all
     constexpr int S = C::RS, NR = C::NR, NC = 3, NROOM = NR * NC;
-    uint8_t dpy[NROOM], dpx[NROOM];  // door_pos[0].y and door_pos[1].x per room
+    static_assert(S == 3, "grids <= 8x8 imply room size 3");
+    // door_pos[0].y / door_pos[1].x draws: _rand_int over a range of S-2 = 1
+    // value, so the positions are fixed, but the draws are consumed
     for (int j = 0; j < NR; ++j)
       for (int i = 0; i < NC; ++i) {
-        const int r = j * NC + i;
-        if (i < NC - 1) dpy[r] = (uint8_t)(j * (S - 1) + 1 + ds.next_bounded(S - 2));
-        if (j < NR - 1) dpx[r] = (uint8_t)(i * (S - 1) + 1 + ds.next_bounded(S - 2));
+        if (i < NC - 1) (void)ds.next();
+        if (j < NR - 1) (void)ds.next();
       }
+    // room links as bit masks over rooms r = 3j + i: H bit r = rooms r, r+1
+    // linked; V bit r = rooms r, r+3 linked (removed walls and doors of any state)
+    uint32_t Hl = 0, Vl = 0;
     const int adx = (NC / 2) * (S - 1) + S / 2, ady = (NR / 2) * (S - 1) + S / 2;  // default agent
-    uint32_t adj[NROOM];
-#pragma unroll
-    for (int r = 0; r < NROOM; ++r) adj[r] = 0;
     // hallway: remove_wall(1, j, up) for j >= 1
     for (int j = 1; j < NR; ++j) {
       for (int t = 1; t < S - 1; ++t) g.set((S - 1) + t, j * (S - 1), CELL_EMPTY);
-      adj[j * NC + 1] |= 1u << ((j - 1) * NC + 1);
-      adj[(j - 1) * NC + 1] |= 1u << (j * NC + 1);
+      Vl |= 1u << ((j - 1) * NC + 1);
     }
     const int room_idx = (int)ds.next_bounded(NR);
     const uint8_t door_col = (uint8_t)ds.next_bounded(6);           // R#23
     const int locked_room = room_idx * NC + 2;
-    g.set(2 * (S - 1), dpy[room_idx * NC + 1], make_cell(K_DOOR_LOCKED, door_col));
-    adj[locked_room] |= 1u << (locked_room - 1);
-    adj[locked_room - 1] |= 1u << locked_room;
+    g.set(2 * (S - 1), room_idx * (S - 1) + 1, make_cell(K_DOOR_LOCKED, door_col));
+    Hl |= 1u << (locked_room - 1);
     // object placement inside room (ri, rj): empty, not the default agent
     // cell, Manhattan distance >= 2 from it (reject_next_to, R#25)
     auto place_in_room = [&](int ri, int rj, uint8_t cell) {
@@ -197,18 +196,20 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
         o.ay = ry + (p >> 2) / S;
       }
     }
-    // connect_all(max_itrs = 5000)
+    // connect_all(max_itrs = 5000): reachability from the agent's room is kept
+    // incrementally (links only grow) and closed bit-parallel over H/V
     const uint32_t all = (1u << NROOM) - 1;
-    const int start = (o.ay / (S - 1)) * NC + o.ax / (S - 1);
+    auto closure = [&](uint32_t reach) {
+      uint32_t prev;
+      do {
+        prev = reach;
+        reach |= ((reach & Hl) << 1) | ((reach >> 1) & Hl) | ((reach & Vl) << NC) | ((reach >> NC) & Vl);
+      } while (reach != prev);
+      return reach;
+    };
+    uint32_t reach = closure(1u << ((o.ay / (S - 1)) * NC + o.ax / (S - 1)));
     for (int it = 0;; ++it) {
       if (it > 5000) { o.fail += 1; break; }
-      uint32_t reach = 1u << start, prev = 0;
-      while (reach != prev) {
-        prev = reach;
-#pragma unroll
-        for (int r = 0; r < NROOM; ++r)
-          if ((reach >> r) & 1u) reach |= adj[r];
-      }
       if (reach == all) break;
       const int i = (int)ds.next_bounded(NC);
       const int j = (int)ds.next_bounded(NR);
@@ -217,17 +218,19 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
       const bool has = k == 0 ? i < NC - 1 : k == 1 ? j < NR - 1 : k == 2 ? i > 0 : j > 0;
       if (!has) continue;
       const int nb = k == 0 ? r + 1 : k == 1 ? r + NC : k == 2 ? r - 1 : r - NC;
-      if ((adj[r] >> nb) & 1u) continue;
+      const int lo = r < nb ? r : nb;  // link bit: the lower room of the pair
+      const bool horiz = (k & 1) == 0;
+      if ((((horiz ? Hl : Vl) >> lo) & 1u)) continue;
       if (r == locked_room || nb == locked_room) continue;
       const uint8_t col = (uint8_t)ds.next_bounded(6);
-      int x, y;
-      if (k == 0) { x = i * (S - 1) + S - 1; y = dpy[r]; }
-      else if (k == 1) { x = dpx[r]; y = j * (S - 1) + S - 1; }
-      else if (k == 2) { x = (i - 1) * (S - 1) + S - 1; y = dpy[r - 1]; }
-      else { x = dpx[r - NC]; y = (j - 1) * (S - 1) + S - 1; }
+      // door_pos[k] of room (i, j) with room size 3
+      const int li = lo % NC, lj = lo / NC;
+      const int x = horiz ? li * (S - 1) + S - 1 : li * (S - 1) + 1;
+      const int y = horiz ? lj * (S - 1) + 1 : lj * (S - 1) + S - 1;
       g.set(x, y, make_cell(K_DOOR_CLOSED, col));
-      adj[r] |= 1u << nb;
-      adj[nb] |= 1u << r;
+      if (horiz) Hl |= 1u << lo;
+      else Vl |= 1u << lo;
+      if (((reach >> r) ^ (reach >> nb)) & 1u) reach = closure(reach);
     }
   }
   return o;

@@ -233,17 +233,33 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
           const uint32_t p = (balls >> (8 * bb)) & 0xFF;
           if (!p) continue;
           const int bx = p >> 4, by = p & 15;
+          // admissible cells of the 3x3 box, row-major bit k = 3*dy + dx: empty
+          // (cell byte == 0x01: a byte permute gathers the 3 cells of each
+          // row, a SWAR exact-zero test finds the empty ones) and not the agent
+          const uint32_t sel = (uint32_t)((bx - 1) | (bx << 4) | ((bx + 1) << 8));
           uint32_t m = 0;
 #pragma unroll
-          for (int k = 0; k < 9; ++k) {
-            const int x = bx - 1 + k % 3, y = by - 1 + k / 3;
-            const bool ok = g.get(x, y) == CELL_EMPTY && !(x == ax && y == ay);
-            m |= (ok ? 1u : 0u) << k;
+          for (int dy = 0; dy < 3; ++dy) {
+            const uint64_t line = rows[(by - 1 + dy) * TILE];
+            const uint32_t x = prmt((uint32_t)line, (uint32_t)(line >> 32), sel) ^ 0x01010101u;
+            const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // bit 7: byte == 0
+            m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (3 * dy);
           }
+          const int adx = ax - (bx - 1), ady = ay - (by - 1);
+          if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (3 * ady + adx));
           if (m) {
             const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
-            const int k = select64(m, bounded(ub, __popc(m)));
-            const int nx = bx - 1 + k % 3, ny = by - 1 + k / 3;
+            uint32_t kk = bounded(ub, __popc(m)), k = 0;  // kk-th set bit of the 9-bit mask
+            uint32_t c = __popc(m & 0xFFu);
+            if (kk >= c) { kk -= c; k = 8; }
+            const uint32_t mm = m >> k;
+            c = __popc(mm & 0xFu);
+            if (kk >= c) { kk -= c; k += 4; }
+            const uint32_t m4 = m >> k;
+            c = __popc(m4 & 0x3u);
+            if (kk >= c) { kk -= c; k += 2; }
+            k += kk >= ((m >> k) & 1u) ? 1u : 0u;
+            const int nx = bx - 1 + (int)(k % 3), ny = by - 1 + (int)(k / 3);
             g.set(nx, ny, make_cell(K_BALL, COL_BLUE));
             g.set(bx, by, CELL_EMPTY);
             balls = (balls & ~(0xFFu << (8 * bb))) | ((uint32_t)((nx << 4) | ny) << (8 * bb));
