@@ -125,6 +125,17 @@ NAVIX_API navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream);
 NAVIX_API navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t* obs, float* reward,
                         uint8_t* terminated, uint8_t* truncated, void* stream);
 
+/* K consecutive steps in ONE launch (the analogue of the
+ * paper's lax.scan over the step, Code 2-3 P:603-660): bit-identical to K
+ * navix_step calls with actions[t], while the environment state stays on chip
+ * between the steps (only actions in, observations / rewards / flags out).
+ *  actions     (dev) uint8[steps][n]
+ *  obs         (dev) uint8[steps][n][7][7][3]   (n % 16 == 0 and a 16-byte
+ *              aligned base enable the per-tile TMA bulk store)
+ *  reward      (dev) float[steps][n];  terminated, truncated (dev) uint8[steps][n] */
+NAVIX_API navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, uint8_t* obs,
+                                     float* reward, uint8_t* terminated, uint8_t* truncated, void* stream);
+
 /* The current observation of every env without stepping (O: S -> O, Table 3). */
 NAVIX_API navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream);
 

@@ -288,6 +288,21 @@ navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t* obs, floa
   return launch(h, MODE_STEP, a, stream);
 }
 
+navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, uint8_t* obs, float* reward,
+                           uint8_t* terminated, uint8_t* truncated, void* stream) {
+  if (!h || !actions || !obs || !reward || !terminated || !truncated)
+    return fail(NAVIX_E_INVALID_ARG, "navix_rollout: null argument");
+  if (steps <= 0) return fail(NAVIX_E_INVALID_ARG, "navix_rollout: steps must be positive (got %lld)", (long long)steps);
+  KernelArgs a = make_args(h);
+  a.actions = actions;
+  a.obs = obs;
+  a.reward = reward;
+  a.terminated = terminated;
+  a.truncated = truncated;
+  a.rollout_steps = steps;
+  return launch(h, MODE_ROLLOUT, a, stream);
+}
+
 navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream) {
   if (!h || !obs) return fail(NAVIX_E_INVALID_ARG, "navix_observe: null argument");
   KernelArgs a = make_args(h);

@@ -113,8 +113,9 @@ struct KernelArgs {
   int reward_mode;
   int bulk_obs;         // 1: obs base is 16-B aligned -> cp.async.bulk store of full tiles
   int bulk_act;         // 1: actions base is 16-B aligned -> cp.async.bulk load of full tiles
+  int64_t rollout_steps;  // K of navix_rollout
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2 };
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3 };
 
 }  // namespace navix

@@ -146,17 +146,52 @@ __device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t ti
 // Per-thread results of a tile, written out by tile_store().
 struct EnvResult {
   float reward;
-  bool valid, regen, term, trunc;
+  bool valid, regen, term, trunc, dirty;
   uint64_t nrec;
   uint32_t episode, balls;
   uint32_t st[8];
 };
 
+// One env's inputs for a step (decoded from the staged tile, or carried in
+// registers across the steps of a rollout).
+struct EnvIn {
+  uint64_t rec;      // agent record
+  uint32_t act;      // action
+  uint32_t balls;    // DynObs ball positions
+  uint32_t episode;  // episode counter
+  bool episode_known;  // else read from HBM when an auto-reset needs it
+};
+
+template <int FAM, int MODE>
+__device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile, const TileSmem<FAM>& b) {
+  const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
+  const int64_t tile0 = tile * TILE, e = tile0 + le;
+  EnvIn in{0, 0, 0, 0, false};
+  if (MODE != MODE_RESET) {
+    in.rec = b.agent[tid];
+    if (MODE == MODE_STEP && e < a.n) {
+      const bool act_bulk = a.bulk_act && tile0 + TILE <= a.n;
+      in.act = act_bulk ? b.act[le] : a.actions[e];
+    }
+    if (FAM == FAM_DYNOBS) {
+      in.balls = b.balls[tid];
+      if (MODE == MODE_STEP) {
+        in.episode = b.episode[tid];
+        in.episode_known = true;
+      }
+    }
+  }
+  return in;
+}
+
 // a1-a6 for this thread's env: compute, then write its obs record into s_obs
-// (after before_emit() has made sure s_obs is free).
+// (after before_emit() has made sure s_obs is free).  rows: this env's 8 SMEM
+// row lines (stride TILE); scratch: 8 more lines for the column view of odd
+// directions, or nullptr to transpose the rows in place (then the rows are
+// written back to HBM first if the grid changed, and are lost).
 template <int FAM, int H, int W, int MODE, class BeforeEmit>
-__device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint8_t* s_obs,
-                                                  BeforeEmit before_emit) {
+__device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t tile, uint64_t* rows, uint64_t* scratch,
+                                                  const EnvIn& in, uint8_t* s_obs, BeforeEmit before_emit) {
   using C = Cfg<FAM, H, W>;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -166,24 +201,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   const int64_t e = tile0 + le;       // env index (caller arrays)
   const bool valid = e < a.n;
   const uint32_t genv = a.env_begin + (uint32_t)e;  // global env index: Philox counter word c0
-  uint64_t* const rows = &b.rows[0][tid];
   RowView g{rows};
 
-  // ---- a1: decode the staged inputs
-  uint8_t act = 0;
-  uint64_t rec = 0;
-  uint32_t balls = 0, episode = 0;
-  if (MODE != MODE_RESET) {
-    rec = b.agent[tid];
-    if (MODE == MODE_STEP && valid) {
-      const bool act_bulk = a.bulk_act && tile0 + TILE <= a.n;
-      act = act_bulk ? b.act[le] : a.actions[e];
-    }
-    if (FAM == FAM_DYNOBS) {
-      balls = b.balls[tid];
-      if (MODE == MODE_STEP) episode = b.episode[tid];
-    }
-  }
+  // ---- a1: inputs
+  uint8_t act = (uint8_t)in.act;
+  const uint64_t rec = in.rec;
+  uint32_t balls = in.balls, episode = in.episode;
   int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
   uint8_t carry = (uint8_t)(rec >> 24);
   uint32_t sc = (uint32_t)((rec >> 32) & 0xFFFF);
@@ -198,7 +221,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   if (regen) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
     if (MODE == MODE_STEP) {
-      if (FAM != FAM_DYNOBS) episode = a.episode[slot];
+      if (!in.episode_known) episode = a.episode[slot];
       episode += 1;
     }
     const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi);
@@ -233,7 +256,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
           const uint32_t p = (balls >> (8 * bb)) & 0xFF;
           if (!p) continue;
           const int bx = p >> 4, by = p & 15;
-          // admissible cells of the 3x3 box, row-major bit k = 3*dy + dx: empty
+          // admissible cells of the 3x3 box, row-major bit k = 4*dy + dx: empty
           // (cell byte == 0x01: a byte permute gathers the 3 cells of each
           // row, a SWAR exact-zero test finds the empty ones) and not the agent
           const uint32_t sel = (uint32_t)((bx - 1) | (bx << 4) | ((bx + 1) << 8));
@@ -243,13 +266,13 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
             const uint64_t line = rows[(by - 1 + dy) * TILE];
             const uint32_t x = prmt((uint32_t)line, (uint32_t)(line >> 32), sel) ^ 0x01010101u;
             const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // bit 7: byte == 0
-            m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (3 * dy);
+            m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (4 * dy);
           }
           const int adx = ax - (bx - 1), ady = ay - (by - 1);
-          if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (3 * ady + adx));
+          if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (4 * ady + adx));
           if (m) {
             const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
-            uint32_t kk = bounded(ub, __popc(m)), k = 0;  // kk-th set bit of the 9-bit mask
+            uint32_t kk = bounded(ub, __popc(m)), k = 0;  // kk-th set bit (row-major order)
             uint32_t c = __popc(m & 0xFFu);
             if (kk >= c) { kk -= c; k = 8; }
             const uint32_t mm = m >> k;
@@ -259,7 +282,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
             c = __popc(m4 & 0x3u);
             if (kk >= c) { kk -= c; k += 2; }
             k += kk >= ((m >> k) & 1u) ? 1u : 0u;
-            const int nx = bx - 1 + (int)(k % 3), ny = by - 1 + (int)(k / 3);
+            const int nx = bx - 1 + (int)(k & 3), ny = by - 1 + (int)(k >> 2);
             g.set(nx, ny, make_cell(K_BALL, COL_BLUE));
             g.set(bx, by, CELL_EMPTY);
             balls = (balls & ~(0xFFu << (8 * bb))) | ((uint32_t)((nx << 4) | ny) << (8 * bb));
@@ -318,7 +341,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   }
 
   // ---- a7a: grid write-back (only when modified), before the lines are reused
-  if (MODE != MODE_OBSERVE && grid_dirty) {
+  if (MODE != MODE_OBSERVE && grid_dirty && scratch == nullptr) {
     uint64_t* gdst = a.grid + tile0 * H + tid;
 #pragma unroll
     for (int y = 0; y < H; ++y)
@@ -326,12 +349,22 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   }
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
-  if (dir & 1) transpose_lines(rows);
+  const uint64_t* lines = rows;
+  if (dir & 1) {
+    if (scratch) {
+#pragma unroll
+      for (int y = 0; y < 8; ++y) scratch[y * TILE] = rows[y * TILE];
+      transpose_lines(scratch);
+      lines = scratch;
+    } else {
+      transpose_lines(rows);
+    }
+  }
   before_emit();
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
-    observe_emit(rows, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
+    observe_emit(lines, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
 
   EnvResult r;
@@ -340,6 +373,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.regen = regen;
   r.term = term;
   r.trunc = trunc;
+  r.dirty = grid_dirty;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
            ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48);
   r.episode = episode;
@@ -370,8 +404,9 @@ __device__ __forceinline__ void store_obs(const KernelArgs& a, int64_t tile, con
   }
 }
 
-// a7: per-env global stores and the episode statistics.
-template <int FAM, int MODE>
+// a7: per-env global stores and the episode statistics (WRITE_STATE = 0 in a
+// rollout, whose state stays on chip until its last step).
+template <int FAM, int MODE, bool WRITE_STATE = true>
 __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, const EnvResult& r) {
   if (MODE == MODE_OBSERVE) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -382,9 +417,11 @@ __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, co
       a.terminated[e] = r.term;
       a.truncated[e] = r.trunc;
     }
-    a.agent[slot] = r.nrec;
-    if (r.regen) a.episode[slot] = r.episode;
-    if (FAM == FAM_DYNOBS) a.balls[slot] = r.balls;
+    if (WRITE_STATE) {
+      a.agent[slot] = r.nrec;
+      if (r.regen) a.episode[slot] = r.episode;
+      if (FAM == FAM_DYNOBS) a.balls[slot] = r.balls;
+    }
   }
   // episode statistics (info i_{t+1}): warp reduce -> striped atomics
   const unsigned any = __any_sync(0xffffffffu, (r.st[0] | r.st[7]) != 0);
@@ -418,7 +455,8 @@ __global__ void __launch_bounds__(TILE, 8) navix_kernel(const KernelArgs a) {
     __syncthreads();  // mbarrier initialised before anyone waits on it
     mbar_wait(mbar, 0);
   }
-  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, s_buf, s_obs, [] {});
+  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, &s_buf.rows[0][threadIdx.x], nullptr,
+                                                    decode_staged<FAM, MODE>(a, blockIdx.x, s_buf), s_obs, [] {});
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   store_obs(a, blockIdx.x, s_obs, threadIdx.x, TILE, threadIdx.x == 0);
@@ -468,7 +506,8 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     // claim the tile-after-next now: the atomic's latency hides behind the compute
     unsigned int next = 0;
     if (tid == 0) next = atomicAdd(&sched[0], 1u);
-    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(a, tile, s_buf[cur], s_obs, [&] {
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(
+        a, tile, &s_buf[cur].rows[0][tid], nullptr, decode_staged<FAM, MODE_STEP>(a, tile, s_buf[cur]), s_obs, [&] {
       if (it > 0) {  // the previous tile's store must have read s_obs
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
@@ -488,6 +527,69 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
       atomicExch(&sched[1], 0u);
     }
   }
+}
+
+// f1: K consecutive steps of one tile in one CTA.  The grid rows
+// stay in SMEM and the agent record, episode and balls in registers across
+// the K steps; per step only the actions come in and obs / reward / flags go
+// out (154 B per DoorKey env-step instead of 234).  Bit-identical to K
+// navix_step calls; outputs of step t at [t][n].
+template <int FAM, int H, int W>
+__global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a, int64_t K) {
+  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
+  __shared__ __align__(128) TileSmem<FAM> s_buf;
+  __shared__ __align__(16) uint64_t s_scratch[8][TILE];
+  __shared__ __align__(8) uint64_t s_mbar;
+  const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
+  const int64_t tile = blockIdx.x, tile0 = tile * TILE, slot = tile0 + tid, e = tile0 + le;
+  const bool valid = e < a.n;
+  const uint32_t mbar = smem_u32(&s_mbar);
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    issue_tile_loads<FAM, H, MODE_OBSERVE>(a, tile, s_buf, mbar);  // rows, agents (+ balls)
+  }
+  __syncthreads();
+  mbar_wait(mbar, 0);
+  EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0u, a.episode[slot], true};
+  bool dirty = false;
+  uint32_t next_act = valid ? a.actions[e] : 0u;
+  for (int64_t t = 0; t < K; ++t) {
+    in.act = next_act;
+    if (t + 1 < K && valid) next_act = a.actions[(t + 1) * a.n + e];  // one step ahead
+    KernelArgs as = a;
+    as.obs = a.obs + t * a.n * OBS_BYTES;
+    as.reward = a.reward + t * a.n;
+    as.terminated = a.terminated + t * a.n;
+    as.truncated = a.truncated + t * a.n;
+    as.bulk_obs = (reinterpret_cast<uintptr_t>(as.obs) & 15u) == 0;
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(as, tile, &s_buf.rows[0][tid], &s_scratch[0][tid], in,
+                                                           s_obs, [&] {
+      if (t > 0) {  // the previous step's store must have read s_obs
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+      }
+    });
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    store_obs(as, tile, s_obs, tid, TILE, tid == 0);
+    tile_store<FAM, MODE_STEP, false>(as, tile, r);
+    in.rec = r.nrec;
+    in.episode = r.episode;
+    in.balls = r.balls;
+    dirty |= r.dirty;
+  }
+  if (valid) {
+    a.agent[slot] = in.rec;
+    a.episode[slot] = in.episode;
+    if (FAM == FAM_DYNOBS) a.balls[slot] = in.balls;
+  }
+  if (dirty) {
+    uint64_t* gdst = a.grid + tile0 * H + tid;
+#pragma unroll
+    for (int y = 0; y < H; ++y)
+      gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : s_buf.rows[y][tid];
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ other kernels
@@ -539,6 +641,8 @@ static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cu
     const int64_t cap = (int64_t)per_sm * n_sm;
     const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
     navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
+  } else if (mode == MODE_ROLLOUT) {
+    navix_rollout_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.rollout_steps);
   } else if (mode == MODE_RESET) {
     navix_kernel<FAM, H, W, MODE_RESET><<<(unsigned)n_tiles, block, 0, s>>>(a);
   } else {

@@ -24,7 +24,7 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
                 "n_lava", "n_collision", "n_truncated", "gen_failures")
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
-    "navix_step", "navix_observe", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_step", "navix_rollout", "navix_observe", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -73,6 +73,7 @@ def load_library():
         "navix_reset": ([P, P, P], I32),
         "navix_step": ([P, P, P, P, P, P, P], I32),
         "navix_observe": ([P, P, P], I32),
+        "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
         "navix_sample_actions": ([P, U64, I64, I64, P, P], I32),
         "navix_step_host": ([P, P, P, P, P, P, P], I32),
         "navix_stats": ([P, P, P], I32),
@@ -179,6 +180,28 @@ class NavixEnv:
         self._check_out(trunc, (self.n,), torch.uint8)
         _check(self.lib.navix_step(self.h, _ptr(actions), _ptr(obs), _ptr(rew), _ptr(term), _ptr(trunc),
                                    _stream(self.device)))
+        return obs, rew, term, trunc
+
+    def rollout(self, actions: torch.Tensor, out=None):
+        """K steps in one launch (state on chip): actions uint8[K, n] ->
+        obs uint8[K, n, 7, 7, 3], reward float32[K, n], terminated / truncated uint8[K, n]."""
+        if actions.dim() != 2:
+            raise ValueError("actions must be uint8[K, n]")
+        K = actions.shape[0]
+        self._check_out(actions, (K, self.n), torch.uint8)
+        dev = self.device
+        if out is None:
+            out = (torch.empty((K, self.n, 7, 7, 3), dtype=torch.uint8, device=dev),
+                   torch.empty((K, self.n), dtype=torch.float32, device=dev),
+                   torch.empty((K, self.n), dtype=torch.uint8, device=dev),
+                   torch.empty((K, self.n), dtype=torch.uint8, device=dev))
+        obs, rew, term, trunc = out
+        self._check_out(obs, (K, self.n, 7, 7, 3), torch.uint8)
+        self._check_out(rew, (K, self.n), torch.float32)
+        self._check_out(term, (K, self.n), torch.uint8)
+        self._check_out(trunc, (K, self.n), torch.uint8)
+        _check(self.lib.navix_rollout(self.h, _ptr(actions), K, _ptr(obs), _ptr(rew), _ptr(term), _ptr(trunc),
+                                      _stream(dev)))
         return obs, rew, term, trunc
 
     def observe(self, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -1,0 +1,51 @@
+"""f1: navix_rollout — K steps in one launch with the state kept
+on chip — must be bit-identical to K navix_step calls (every output of every
+step, the final canonical state, the statistics), and to the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from inputgen import random_actions
+from oracle import OracleEnv
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("env_id,n,K", [
+    ("DoorKey-8x8-v0", 4096, 96), ("Dynamic-Obstacles-8x8-v0", 1000, 80), ("KeyCorridorS3R3-v0", 777, 300),
+    ("LavaGapS7-v0", 513, 120), ("Empty-5x5-v0", 16, 250), ("DoorKey-5x5-v0", 129, 64),
+    ("KeyCorridorS3R1-v0", 200, 290)])
+def test_rollout_equals_sequential_steps(env_id, n, K):
+    from paper_2407_19396_b200 import NavixEnv
+    a = NavixEnv(env_id, n, seed=8)
+    b = NavixEnv(env_id, n, seed=8)
+    a.reset()
+    b.reset()
+    acts = torch.from_numpy(random_actions(6, 2 * K, n, 0, high=8)).cuda()
+    for half in range(2):  # two consecutive rollouts: state carried over between launches
+        ro, rr, rte, rtr = a.rollout(acts[half * K:(half + 1) * K].contiguous())
+        for t in range(K):
+            o, r, te, tr = b.step(acts[half * K + t])
+            assert torch.equal(ro[t], o), (half, t)
+            assert torch.equal(rr[t].view(torch.int32), r.view(torch.int32))
+            assert torch.equal(rte[t], te) and torch.equal(rtr[t], tr)
+        assert np.array_equal(a.export_state(), b.export_state())
+    assert torch.equal(a.stats(), b.stats())
+
+
+def test_rollout_matches_oracle():
+    from paper_2407_19396_b200 import NavixEnv
+    n, K = 2048, 200
+    g = NavixEnv("DoorKey-8x8-v0", n, seed=3)
+    o = OracleEnv("DoorKey-8x8-v0", n, seed=3)
+    g.reset()
+    o.reset()
+    acts = random_actions(2, K, n, 7)
+    ro, rr, rte, rtr = g.rollout(torch.from_numpy(acts).cuda())
+    for t in range(K):
+        oo, orw, ote, otr = o.step(acts[t])
+        assert np.array_equal(ro[t].cpu().numpy(), oo), t
+        assert np.array_equal(rr[t].cpu().numpy().view(np.uint32), orw.view(np.uint32))
+        assert np.array_equal(rte[t].cpu().numpy(), ote) and np.array_equal(rtr[t].cpu().numpy(), otr)
+    assert np.array_equal(g.export_state(), o.export())
+    assert np.array_equal(g.stats().cpu().numpy(), o.stats())
