@@ -278,6 +278,33 @@ def run_navix(args, rank, world, local_rank):
     # episode statistics: the one collective of the path (NCCL all-reduce of int64[8])
     st = all_reduce_stats(env.stats()).cpu().numpy()
 
+    # f1: fused K-step rollout (navix_rollout), same envs and random policy
+    rollout = None
+    if args.rollout_steps > 0:
+        Kr = args.rollout_steps
+        r_acts = acts[:Kr] if Kr <= ring else env.sample_actions(1, 0, Kr)
+        outs = (torch.empty((Kr, n, 7, 7, 3), dtype=torch.uint8, device=dev),
+                torch.empty((Kr, n), dtype=torch.float32, device=dev),
+                torch.empty((Kr, n), dtype=torch.uint8, device=dev),
+                torch.empty((Kr, n), dtype=torch.uint8, device=dev))
+        env.rollout(r_acts, out=outs)  # warm-up
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        r0.record(s)
+        for _ in range(reps):
+            env.rollout(r_acts, out=outs)
+        r1.record(s)
+        torch.cuda.synchronize(dev)
+        t_r = max_over_ranks(r0.elapsed_time(r1) / 1e3 / reps, dev)
+        Br = 1 + 147 + 4 + 2
+        rollout = {"steps_per_launch": Kr, "value": n_total * Kr / t_r, "unit": UNIT,
+                   "ms_per_launch": 1e3 * t_r, "algorithmic_bytes_per_env_step": Br,
+                   "achieved_GBps_per_gpu": Br * n * Kr / t_r / 1e9,
+                   "frac_of_measured_hbm": Br * n * Kr / t_r / 1e9 / measured_peaks()[0],
+                   "api": "navix_rollout (state on chip across the K steps; row f1)"}
+        del outs
+
     # end to end through the host-buffer C-ABI call (H2D actions, D2H outputs)
     h_act = torch.from_numpy(np.ascontiguousarray(acts[: args.e2e_steps].cpu().numpy())).pin_memory()
     h_obs = torch.empty((n, 7, 7, 3), dtype=torch.uint8).pin_memory()
@@ -325,6 +352,7 @@ def run_navix(args, rank, world, local_rank):
                 "d2h_bytes_per_step": n_total * (147 + 4 + 1 + 1), "steps": args.e2e_steps,
                 "api": "navix_step_host (pinned host buffers)"},
         "gpu_launches": args.steps,
+        "rollout": rollout,
         "clocks": clk.summary(),
         "episode_stats": {k: int(v) for k, v in zip(
             ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_collision", "n_truncated",
@@ -348,6 +376,7 @@ def main():
     ap.add_argument("--envs-per-gpu", type=int, default=1 << 20)
     ap.add_argument("--action-ring", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--rollout-steps", type=int, default=64)
     ap.add_argument("--cpu-envs", type=int, default=4096)
     ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
