@@ -218,7 +218,44 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
            st_fail = 0;
 
   const bool regen = MODE == MODE_RESET || (MODE == MODE_STEP && prev_done);
-  if (regen) {
+  // Dynamic-Obstacles auto-resets ~10 % of its envs per step: left in place,
+  // nearly every warp would run the level generator for a few lanes.  Its
+  // resetting envs are queued per CTA instead and generated by the first
+  // threads (one warp for up to 32 of them), each into its env's SMEM rows.
+  constexpr bool COMPACT = FAM == FAM_DYNOBS && MODE == MODE_STEP;
+  if (COMPACT) {
+    __shared__ int s_qn;
+    __shared__ int s_q[TILE];
+    __shared__ uint32_t s_qep[TILE];
+    __shared__ uint64_t s_qout[TILE];
+    if (tid == 0) s_qn = 0;
+    __syncthreads();
+    if (regen) {
+      s_q[atomicAdd(&s_qn, 1)] = tid;
+      s_qep[tid] = (in.episode_known ? episode : a.episode[slot]) + 1;
+    }
+    __syncthreads();
+    const int nq = s_qn;
+    for (int q = tid; q < nq; q += TILE) {
+      const int st = s_q[q];
+      const uint32_t genv_t = a.env_begin + (uint32_t)(tile0 + env_of_slot(st));
+      const GenOut o = generate_level<FAM, H, W>(RowView{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi);
+      s_qout[st] = (uint64_t)o.balls | ((uint64_t)o.ax << 32) | ((uint64_t)o.ay << 40) | ((uint64_t)o.dir << 48) |
+                   ((uint64_t)o.fail << 56);
+    }
+    __syncthreads();
+    if (regen) {
+      const uint64_t o = s_qout[tid];
+      episode = s_qep[tid];
+      balls = (uint32_t)o;
+      ax = (int)((o >> 32) & 0xFF); ay = (int)((o >> 40) & 0xFF); dir = (int)((o >> 48) & 3);
+      st_fail = (uint32_t)(o >> 56);
+      carry = CELL_EMPTY;
+      sc = 0;
+      prev_done = false;
+      grid_dirty = true;
+    }
+  } else if (regen) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
     if (MODE == MODE_STEP) {
       if (!in.episode_known) episode = a.episode[slot];
@@ -232,7 +269,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     sc = 0;
     prev_done = false;
     grid_dirty = true;
-  } else {
+  }
+  if (!regen) {
     if (FAM == FAM_DYNOBS) {
 #pragma unroll
       for (int bb = 0; bb < C::NOBST; ++bb) {
