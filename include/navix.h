@@ -136,6 +136,18 @@ NAVIX_API navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t*
 NAVIX_API navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, uint8_t* obs,
                                      float* reward, uint8_t* terminated, uint8_t* truncated, void* stream);
 
+/* Reward composition (Table 6 `time_cost`, `action_cost`; Code 4 `compose`,
+ * P:673-680; R#31): every later step adds -time_cost, and
+ * -action_cost unless the action is done (6), to the event reward, in binary32
+ * in that order.  Auto-reset calls still return 0.  Both >= 0; 0 disables.
+ * Host only, takes effect for subsequently enqueued steps. */
+NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost);
+
+/* Table 5 `symbolic` full-grid observation, MiniGrid's
+ * FullyObsWrapper: out (dev) uint8[n][width][height][3] ([x][y][c]), every
+ * cell encoded (type, colour, state) and the agent cell (10, 0, dir) (R#32). */
+NAVIX_API navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream);
+
 /* The current observation of every env without stepping (O: S -> O, Table 3). */
 NAVIX_API navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream);
 

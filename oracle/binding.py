@@ -57,6 +57,8 @@ def oracle_lib():
     lib.oracle_sample_actions.argtypes = [U64, I64, I64, I64, I64, I32, P]
     lib.oracle_process_vis7.argtypes = [P, P]
     lib.oracle_view_tags.argtypes = [I32, I32, I32, I32, I32, P]
+    lib.oracle_set_reward_costs.argtypes = [P, ctypes.c_float, ctypes.c_float]
+    lib.oracle_observe_full.argtypes = [P, P]
     lib.oracle_success_reward.argtypes = [I32, I32, I32]
     lib.oracle_success_reward.restype = ctypes.c_float
     _lib = lib
@@ -167,6 +169,15 @@ class OracleEnv:
         obs = np.zeros((self.n, 7, 7, 3), np.uint8)
         self.lib.oracle_observe(self.h, _ptr(obs))
         return obs
+
+    def set_reward_costs(self, time_cost: float, action_cost: float) -> None:
+        self.lib.oracle_set_reward_costs(self.h, time_cost, action_cost)
+
+    def observe_full(self) -> np.ndarray:
+        s = self.spec
+        out = np.zeros((self.n, s.width, s.height, 3), np.uint8)
+        self.lib.oracle_observe_full(self.h, _ptr(out))
+        return out
 
     def export(self) -> np.ndarray:
         buf = np.zeros(self.n * self.spec.export_bytes, np.uint8)

@@ -83,6 +83,18 @@ void oracle_observe(void* hp, uint8_t* obs) {
   for (size_t i = 0; i < h->envs.size(); ++i) h->envs[i].gen_obs(obs + i * 147);
 }
 
+void oracle_set_reward_costs(void* hp, float time_cost, float action_cost) {
+  Handle* h = (Handle*)hp;
+  for (auto& e : h->envs) { e.time_cost = time_cost; e.action_cost = action_cost; }
+}
+
+// out[i] = uint8[width][height][3] full-grid symbolic observation of env i.
+void oracle_observe_full(void* hp, uint8_t* out) {
+  Handle* h = (Handle*)hp;
+  const size_t per = (size_t)h->spec.width * h->spec.height * 3;
+  for (size_t i = 0; i < h->envs.size(); ++i) h->envs[i].gen_full_obs(out + i * per);
+}
+
 int64_t oracle_export(void* hp, uint8_t* buf, int64_t cap) {
   Handle* h = (Handle*)hp;
   int64_t per = export_bytes_per_env(h->spec);

@@ -376,6 +376,14 @@ StepOut Env::step(int action) {
     success = false;
   }
   bool truncated = (step_count >= S.max_steps) && !terminated;  // R#17
+  // Code 4 `compose` of the event reward with time_cost (every step) and
+  // action_cost (every action but done), summed in binary32 in this order (R#31)
+  if (time_cost != 0.f || action_cost != 0.f) {
+    volatile float r = reward;
+    r = r + (-time_cost);
+    r = r + (action != A_DONE ? -action_cost : 0.f);
+    reward = r;
+  }
   out.reward = reward;
   out.terminated = terminated;
   out.truncated = truncated;
@@ -409,6 +417,19 @@ void Env::gen_obs(uint8_t* out) const {
   // the agent sees what it carries (R#13)
   g.set(R / 2, R - 1, carrying);
   g.encode(vis, out);
+}
+
+// Table 5 `symbolic`: [MG] FullyObsWrapper — grid.encode() over the
+// whole grid (every cell visible) with the agent cell overwritten by
+// (OBJECT_TO_IDX["agent"], COLOR_TO_IDX["red"], agent_dir); memory order
+// [x][y][c] as Grid.encode returns it (R#32).
+void Env::gen_full_obs(uint8_t* out) const {
+  std::vector<uint8_t> all((size_t)grid.width * grid.height, 1);
+  grid.encode(all, out);
+  uint8_t* a = out + ((size_t)agent_x * grid.height + agent_y) * 3;
+  a[0] = T_AGENT;
+  a[1] = C_RED;
+  a[2] = (uint8_t)agent_dir;
 }
 
 // ---------------------------------------------------------------- export

@@ -122,6 +122,7 @@ struct StepOut {
 struct Env {
   Spec spec;
   int reward_mode = RM_MINIGRID;
+  float time_cost = 0.f, action_cost = 0.f;  // Table 6 time_cost / action_cost (R#31)
   uint64_t seed = 0;
   uint32_t global_index = 0;  // c0 of every Philox counter (shard invariance)
   Grid grid{1, 1};
@@ -137,6 +138,7 @@ struct Env {
   void generate();  // P0 for episode `episode` (levels.cpp)
   StepOut step(int action);
   void gen_obs(uint8_t* out147) const;
+  void gen_full_obs(uint8_t* out) const;  // Table 5 `symbolic`, [x][y][c] (R#32)
   std::pair<int, int> front_pos() const;
 };
 

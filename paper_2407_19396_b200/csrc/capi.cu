@@ -31,6 +31,7 @@ struct navix_env {
   uint64_t seed;
   int device;
   int reward_mode;
+  float time_cost = 0.f, action_cost = 0.f;
   uint8_t* state;
   bool owns_state;
   // navix_step_host staging (lazily allocated)
@@ -131,6 +132,8 @@ KernelArgs make_args(navix_env* h) {
   a.key_lo = (uint32_t)h->seed;
   a.key_hi = (uint32_t)(h->seed >> 32);
   a.reward_mode = h->reward_mode;
+  a.time_cost = h->time_cost;
+  a.action_cost = h->action_cost;
   return a;
 }
 
@@ -301,6 +304,22 @@ navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, 
   a.truncated = truncated;
   a.rollout_steps = steps;
   return launch(h, MODE_ROLLOUT, a, stream);
+}
+
+navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost) {
+  if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_reward_costs: null handle");
+  if (!(time_cost >= 0.f && time_cost < 1e30f) || !(action_cost >= 0.f && action_cost < 1e30f))
+    return fail(NAVIX_E_INVALID_ARG, "reward costs must be finite and >= 0");
+  h->time_cost = time_cost;
+  h->action_cost = action_cost;
+  return NAVIX_OK;
+}
+
+navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream) {
+  if (!h || !out) return fail(NAVIX_E_INVALID_ARG, "navix_observe_full: null argument");
+  KernelArgs a = make_args(h);
+  a.obs = out;
+  return launch(h, MODE_FULL_OBS, a, stream);
 }
 
 navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream) {

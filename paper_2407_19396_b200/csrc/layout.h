@@ -111,11 +111,12 @@ struct KernelArgs {
   uint32_t env_begin;   // global index of local env 0 (Philox counter word c0)
   uint32_t key_lo, key_hi;
   int reward_mode;
+  float time_cost, action_cost;  // Table 6 time_cost / action_cost, composed with the event reward (R#31)
   int bulk_obs;         // 1: obs base is 16-B aligned -> cp.async.bulk store of full tiles
   int bulk_act;         // 1: actions base is 16-B aligned -> cp.async.bulk load of full tiles
   int64_t rollout_steps;  // K of navix_rollout
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3 };
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };
 
 }  // namespace navix

@@ -363,6 +363,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       if (coll) reward = -1.0f;
       else if (__builtin_expect(success, 0)) reward = success_reward(a.reward_mode, sc, C::T);
       else if (lava) reward = a.reward_mode == 1 ? -1.0f : 0.0f;
+      // Code 4 `compose`: + (-time_cost) every step, + (-action_cost) for every
+      // action but done, in binary32 in this order (R#31)
+      if (a.time_cost != 0.f || a.action_cost != 0.f) {
+        reward = __fadd_rn(reward, -a.time_cost);
+        reward = __fadd_rn(reward, act != 6 ? -a.action_cost : 0.f);
+      }
       term = success || lava || coll;
       trunc = sc >= (uint32_t)C::T && !term;
       prev_done = term || trunc;
@@ -630,6 +636,51 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// f3 (Table 5 `symbolic`): the full-grid encoding of MiniGrid's
+// FullyObsWrapper — every cell (type, colour, state), the agent cell replaced
+// by (10 agent, 0 red, dir); memory order [x][y][c] (R#32).  Not on the step
+// path: one thread per env, staged in SMEM, coalesced copy-out.
+template <int FAM, int H, int W>
+__global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint8_t* out) {
+  constexpr int PER = 3 * W * H;
+  __shared__ __align__(16) uint8_t s_out[TILE * PER];
+  const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE, slot = tile0 + tid;
+  const uint64_t rec = a.agent[slot];
+  uint64_t rows[H];
+#pragma unroll
+  for (int y = 0; y < H; ++y) rows[y] = a.grid[tile0 * H + y * TILE + tid];
+  if (FAM == FAM_DYNOBS) {
+    const uint32_t bl = a.balls[slot];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t p = (bl >> (8 * b)) & 0xFF;
+#pragma unroll
+      for (int y = 0; y < H; ++y)
+        if (p && (int)(p & 15) == y)
+          rows[y] = (rows[y] & ~(0xFFull << (8 * (p >> 4)))) | ((uint64_t)make_cell(K_BALL, COL_BLUE) << (8 * (p >> 4)));
+    }
+  }
+  const int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
+  uint8_t* o = s_out + le * PER;
+#pragma unroll
+  for (int y = 0; y < H; ++y)
+#pragma unroll
+    for (int x = 0; x < W; ++x) {
+      const uint32_t c = (uint32_t)(rows[y] >> (8 * x)) & 0xFF, kind = c & 15;
+      uint8_t* t = o + (x * H + y) * 3;
+      const bool ag = x == ax && y == ay;
+      t[0] = ag ? 10 : (kind >= 11 ? 4 : kind);
+      t[1] = ag ? 0 : (c >> 4) & 7;
+      t[2] = ag ? dir : (kind >= 11 ? kind - 10 : 0);
+    }
+  __syncthreads();
+  const int64_t nv = a.n - tile0;
+  const int nvalid = nv >= TILE ? TILE : (int)nv;
+  uint8_t* dst = out + tile0 * PER;
+  for (int i = tid; i < nvalid * PER; i += TILE) dst[i] = s_out[i];
+}
+
 // ------------------------------------------------------------------ other kernels
 __global__ void sample_actions_kernel(uint8_t* out, int64_t n, int64_t steps, uint32_t env_begin, uint32_t t0,
                                       uint32_t klo, uint32_t khi, uint32_t n_actions) {
@@ -679,6 +730,8 @@ static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cu
     const int64_t cap = (int64_t)per_sm * n_sm;
     const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
     navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
+  } else if (mode == MODE_FULL_OBS) {
+    full_obs_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
   } else if (mode == MODE_ROLLOUT) {
     navix_rollout_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.rollout_steps);
   } else if (mode == MODE_RESET) {

@@ -24,7 +24,7 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
                 "n_lava", "n_collision", "n_truncated", "gen_failures")
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
-    "navix_step", "navix_rollout", "navix_observe", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -74,6 +74,8 @@ def load_library():
         "navix_step": ([P, P, P, P, P, P, P], I32),
         "navix_observe": ([P, P, P], I32),
         "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
+        "navix_observe_full": ([P, P, P], I32),
+        "navix_set_reward_costs": ([P, ctypes.c_float, ctypes.c_float], I32),
         "navix_sample_actions": ([P, U64, I64, I64, P, P], I32),
         "navix_step_host": ([P, P, P, P, P, P, P], I32),
         "navix_stats": ([P, P, P], I32),
@@ -203,6 +205,18 @@ class NavixEnv:
         _check(self.lib.navix_rollout(self.h, _ptr(actions), K, _ptr(obs), _ptr(rew), _ptr(term), _ptr(trunc),
                                       _stream(dev)))
         return obs, rew, term, trunc
+
+    def set_reward_costs(self, time_cost: float = 0.0, action_cost: float = 0.0) -> None:
+        """Compose -time_cost per step and -action_cost per non-done action (Table 6)."""
+        _check(self.lib.navix_set_reward_costs(self.h, time_cost, action_cost))
+
+    def observe_full(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Table 5 `symbolic`: uint8[n, width, height, 3], agent cell (10, 0, dir)."""
+        s = self.spec
+        o = torch.empty((self.n, s.width, s.height, 3), dtype=torch.uint8, device=self.device) if out is None else out
+        self._check_out(o, (self.n, s.width, s.height, 3), torch.uint8)
+        _check(self.lib.navix_observe_full(self.h, _ptr(o), _stream(self.device)))
+        return o
 
     def observe(self, out: torch.Tensor | None = None) -> torch.Tensor:
         obs = self.obs if out is None else out

@@ -1,0 +1,59 @@
+"""GPU <-> oracle parity of the f3/f4 variants: reward costs composed with
+the event rewards (step and rollout paths) and the full-grid observation."""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from inputgen import random_actions, random_records
+from oracle import OracleEnv
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("env_id,mode", [("DoorKey-8x8-v0", 0), ("LavaGapS7-v0", 1),
+                                         ("Dynamic-Obstacles-8x8-v0", 0), ("KeyCorridorS3R3-v0", 1)])
+def test_reward_costs_parity(env_id, mode):
+    from paper_2407_19396_b200 import NavixEnv
+    n, K = 700, 150
+    g = NavixEnv(env_id, n, seed=2, reward_mode=mode)
+    r = NavixEnv(env_id, n, seed=2, reward_mode=mode)
+    o = OracleEnv(env_id, n, seed=2, reward_mode=mode)
+    g.set_reward_costs(0.0125, 0.003)
+    r.set_reward_costs(0.0125, 0.003)
+    o.set_reward_costs(0.0125, 0.003)
+    g.reset()
+    r.reset()
+    o.reset()
+    acts = random_actions(9, K, n, 0, high=8)
+    ro, rr, rte, rtr = r.rollout(torch.from_numpy(acts).cuda())
+    for t in range(K):
+        go, gr, gte, gtr = g.step(torch.from_numpy(acts[t]).cuda())
+        oo, orw, ote, otr = o.step(acts[t])
+        assert np.array_equal(gr.cpu().numpy().view(np.uint32), orw.view(np.uint32)), t
+        assert np.array_equal(rr[t].cpu().numpy().view(np.uint32), orw.view(np.uint32)), t
+        assert np.array_equal(gte.cpu().numpy(), ote) and np.array_equal(go.cpu().numpy(), oo)
+
+
+@pytest.mark.parametrize("env_id,nob", [("DoorKey-8x8-v0", 0), ("KeyCorridorS3R3-v0", 0),
+                                        ("Dynamic-Obstacles-8x8-v0", 4), ("Empty-5x5-v0", 0),
+                                        ("KeyCorridorS3R1-v0", 0), ("LavaGapS6-v0", 0)])
+def test_full_obs_parity(env_id, nob):
+    from paper_2407_19396_b200 import NavixEnv
+    n = 1500
+    g = NavixEnv(env_id, n, seed=4)
+    o = OracleEnv(env_id, n, seed=4)
+    g.reset()
+    o.reset()
+    np.testing.assert_array_equal(g.observe_full().cpu().numpy(), o.observe_full())
+    s = g.spec
+    recs = random_records(zlib.crc32(env_id.encode()) % 997, n, s.height, s.width, s.max_steps, nob)
+    g.import_state(recs)
+    o.import_(recs)
+    np.testing.assert_array_equal(g.observe_full().cpu().numpy(), o.observe_full())
+    acts = random_actions(1, 20, n, 0, high=8)
+    for t in range(20):
+        g.step(torch.from_numpy(acts[t]).cuda())
+        o.step(acts[t])
+    np.testing.assert_array_equal(g.observe_full().cpu().numpy(), o.observe_full())
