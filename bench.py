@@ -331,7 +331,7 @@ def run_navix(args, rank, world, local_rank):
     traffic = committed_traffic(args.env)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": None if traffic is None else traffic * n,
-            "algorithmic_bytes_per_env_step": B, "envs_per_launch": n, "kernel": "navix_kernel<DoorKey,8,8,STEP>",
+            "algorithmic_bytes_per_env_step": B, "envs_per_launch": n, "kernel": f"navix_step_persistent<{args.env}>",
             "peak_source": peak_src}
     model, ncpu = cpu_info()
     cpu = None
