@@ -103,7 +103,7 @@ int parse_id(const char* env_id, EnvConfig* c) {
   } else {
     return 1;
   }
-  return (c->height <= 8 && c->width <= 8) ? 0 : 2;
+  return (c->height <= 16 && c->width <= 16) ? 0 : 2;
 }
 
 void fill_spec(const EnvConfig& c, navix_spec* s) {
@@ -124,7 +124,7 @@ KernelArgs make_args(navix_env* h) {
   a.grid = reinterpret_cast<uint64_t*>(s + h->layout.grid_off);
   a.agent = reinterpret_cast<uint64_t*>(s + h->layout.agent_off);
   a.episode = reinterpret_cast<uint32_t*>(s + h->layout.episode_off);
-  a.balls = reinterpret_cast<uint32_t*>(s + h->layout.balls_off);
+  a.balls = reinterpret_cast<uint64_t*>(s + h->layout.balls_off);
   a.stats = reinterpret_cast<unsigned long long*>(s + h->layout.stats_off);
   a.sched = reinterpret_cast<unsigned int*>(s + h->layout.sched_off);
   a.n = h->n;
@@ -187,7 +187,7 @@ navix_status navix_spec_of(const char* env_id, navix_spec* out) {
   if (r == 1) return fail(NAVIX_E_UNKNOWN_ENV, "unknown env id '%s' (Table 9 ids, e.g. Navix-DoorKey-8x8-v0)",
                           env_id ? env_id : "(null)");
   fill_spec(c, out);
-  if (r == 2) return fail(NAVIX_E_UNSUPPORTED, "env id '%s' has a %dx%d grid; this build supports <= 8x8",
+  if (r == 2) return fail(NAVIX_E_UNSUPPORTED, "env id '%s' has a %dx%d grid; this build supports <= 16x16",
                           env_id, c.height, c.width);
   return NAVIX_OK;
 }
@@ -391,8 +391,10 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
   if (cap < need) return fail(NAVIX_E_INVALID_ARG, "export buffer too small (%zu < %zu)", cap, need);
   DeviceGuard dg(h->device);
   const StateLayout& L = h->layout;
-  std::vector<uint64_t> grid((size_t)L.n_pad * c.height), agent((size_t)L.n_pad);
-  std::vector<uint32_t> episode((size_t)L.n_pad), balls(c.family == FAM_DYNOBS ? (size_t)L.n_pad : 0);
+  const int RW = row_planes(c.width), HP = c.height * RW;
+  std::vector<uint64_t> grid((size_t)L.n_pad * HP), agent((size_t)L.n_pad);
+  std::vector<uint32_t> episode((size_t)L.n_pad);
+  std::vector<uint64_t> balls(c.family == FAM_DYNOBS ? (size_t)L.n_pad : 0);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
   if ((e = cudaMemcpy(grid.data(), h->state + L.grid_off, grid.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
@@ -402,19 +404,18 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
           cudaSuccess)
     return cuda_fail(e, "export D2H");
   if (!balls.empty() &&
-      (e = cudaMemcpy(balls.data(), h->state + L.balls_off, balls.size() * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+      (e = cudaMemcpy(balls.data(), h->state + L.balls_off, balls.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
     return cuda_fail(e, "export D2H balls");
   uint8_t* o = static_cast<uint8_t*>(host);
   for (int64_t i = 0; i < h->n; ++i) {
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
-    uint8_t cells[8][8];
-    for (int y = 0; y < c.height; ++y) {
-      const uint64_t row = grid[(size_t)(tile * c.height + y) * TILE + lane];
-      for (int x = 0; x < c.width; ++x) cells[y][x] = (uint8_t)(row >> (8 * x));
-    }
+    uint8_t cells[16][16];
+    for (int y = 0; y < c.height; ++y)
+      for (int x = 0; x < c.width; ++x)
+        cells[y][x] = (uint8_t)(grid[(size_t)(tile * HP + y * RW + x / 8) * TILE + lane] >> (8 * (x % 8)));
     if (c.family == FAM_DYNOBS)
       for (int b = 0; b < c.n_obstacles; ++b) {
-        const uint32_t p = (balls[si] >> (8 * b)) & 0xFF;
+        const uint32_t p = (uint32_t)(balls[si] >> (8 * b)) & 0xFF;
         if (p) cells[p & 15][p >> 4] = make_cell(K_BALL, COL_BLUE);
       }
     uint8_t* p = o + (size_t)i * per;
@@ -434,7 +435,7 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     p[11] = (uint8_t)((r >> 48) & 1);
     p += 12;
     for (int b = 0; b < c.n_obstacles; ++b, p += 2) {
-      const uint32_t q = (balls[si] >> (8 * b)) & 0xFF;
+      const uint32_t q = (uint32_t)(balls[si] >> (8 * b)) & 0xFF;
       p[0] = (uint8_t)(q >> 4);
       p[1] = (uint8_t)(q & 15);
     }
@@ -449,13 +450,13 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
   if (n_bytes != per * (size_t)h->n)
     return fail(NAVIX_E_INVALID_ARG, "import size %zu != %lld envs x %zu bytes", n_bytes, (long long)h->n, per);
   const StateLayout& L = h->layout;
-  const int H = c.height, W = c.width;
-  std::vector<uint64_t> grid((size_t)L.n_pad * H, 0), agent((size_t)L.n_pad, 0);
-  std::vector<uint32_t> episode((size_t)L.n_pad, 0), balls((size_t)L.n_pad, 0);
+  const int H = c.height, W = c.width, RW = row_planes(W);
+  std::vector<uint64_t> grid((size_t)L.n_pad * H * RW, 0), agent((size_t)L.n_pad, 0), balls((size_t)L.n_pad, 0);
+  std::vector<uint32_t> episode((size_t)L.n_pad, 0);
   const uint8_t* in = static_cast<const uint8_t*>(host);
   for (int64_t i = 0; i < h->n; ++i) {
     const uint8_t* p = in + (size_t)i * per;
-    uint8_t cells[8][8] = {};
+    uint8_t cells[16][16] = {};
     for (int y = 0; y < H; ++y)
       for (int x = 0; x < W; ++x, p += 3) {
         if (!to_cell(p, &cells[y][x]))
@@ -481,27 +482,25 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
     if (sc > (uint32_t)c.max_steps || pd > 1)
       return fail(NAVIX_E_INVALID_ARG, "env %lld: step_count %u / prev_done %u out of range", (long long)i, sc, pd);
     p += 12;
-    uint32_t bl = 0;
+    uint64_t bl = 0;
     for (int b = 0; b < c.n_obstacles; ++b, p += 2) {
       const int bx = p[0], by = p[1];
       if (bx < 1 || by < 1 || bx > W - 2 || by > H - 2 || cells[by][bx] != make_cell(K_BALL, COL_BLUE))
         return fail(NAVIX_E_INVALID_ARG, "env %lld: obstacle %d at (%d,%d) is not a blue ball", (long long)i, b, bx,
                     by);
       for (int q = 0; q < b; ++q)
-        if (((bl >> (8 * q)) & 0xFF) == (uint32_t)((bx << 4) | by))
+        if (((bl >> (8 * q)) & 0xFF) == (uint64_t)((bx << 4) | by))
           return fail(NAVIX_E_INVALID_ARG, "env %lld: duplicate obstacle", (long long)i);
-      bl |= (uint32_t)((bx << 4) | by) << (8 * b);
+      bl |= (uint64_t)((bx << 4) | by) << (8 * b);
     }
     for (int b = 0; b < c.n_obstacles; ++b) {  // balls live outside the HBM grid
-      const uint32_t q = (bl >> (8 * b)) & 0xFF;
+      const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
       cells[q & 15][q >> 4] = CELL_EMPTY;
     }
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
-    for (int y = 0; y < H; ++y) {
-      uint64_t row = 0;
-      for (int x = 0; x < W; ++x) row |= (uint64_t)cells[y][x] << (8 * x);
-      grid[(size_t)(tile * H + y) * TILE + lane] = row;
-    }
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x)
+        grid[(size_t)(tile * H * RW + y * RW + x / 8) * TILE + lane] |= (uint64_t)cells[y][x] << (8 * (x % 8));
     agent[si] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
                ((uint64_t)sc << 32) | ((uint64_t)pd << 48);
     episode[si] = ep;
@@ -517,7 +516,7 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
           cudaSuccess)
     return cuda_fail(e, "import H2D");
   if (c.family == FAM_DYNOBS &&
-      (e = cudaMemcpy(h->state + L.balls_off, balls.data(), balls.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+      (e = cudaMemcpy(h->state + L.balls_off, balls.data(), balls.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cuda_fail(e, "import H2D balls");
   return NAVIX_OK;
 }

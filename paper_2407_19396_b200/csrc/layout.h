@@ -1,11 +1,13 @@
 // layout.h — internal data layout of libnavix (host + device).
 //
 // HBM state of one handle (one shard), a single allocation:
-//   grid    u64 [n_tiles][H][TILE]   row y of env (tile, lane): 8 cell bytes,
-//                                     byte x = cell (x, y); bytes x >= W are 0
+//   grid    u64 [n_tiles][H*RW][TILE] row y of env (tile, slot) as RW planes
+//                                     (RW = 1 up to width 8, 2 up to 16): byte
+//                                     x % 8 of plane y*RW + x/8 = cell (x, y);
+//                                     cells x >= W are 0
 //   agent   u64 [n_pad]               agent record (below)
 //   episode u32 [n_pad]               episode counter (counter word c1, R#20)
-//   balls   u32 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b
+//   balls   u64 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b (<= 8)
 //   stats   u64 [NSLOT][8]            striped int64 episode statistics
 //   sched   u32 [2]                   persistent step kernel tile scheduler
 // n_pad = num_envs rounded up to TILE.  The struct-of-arrays "row plane"
@@ -68,19 +70,22 @@ struct StateLayout {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// u64 planes per grid row: 8-byte rows up to width 8, 16-byte rows up to 16 (row f2)
+__host__ __device__ constexpr int row_planes(int width) { return width > 8 ? 2 : 1; }
+
 inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   StateLayout L{};
   L.n_tiles = (n + TILE - 1) / TILE;
   L.n_pad = L.n_tiles * TILE;
   size_t off = 0;
   L.grid_off = off;
-  off = align_up(off + (size_t)L.n_pad * c.height * 8, 256);
+  off = align_up(off + (size_t)L.n_pad * c.height * row_planes(c.width) * 8, 256);
   L.agent_off = off;
   off = align_up(off + (size_t)L.n_pad * 8, 256);
   L.episode_off = off;
   off = align_up(off + (size_t)L.n_pad * 4, 256);
   L.balls_off = off;
-  off = align_up(off + (c.family == FAM_DYNOBS ? (size_t)L.n_pad * 4 : 0), 256);
+  off = align_up(off + (c.family == FAM_DYNOBS ? (size_t)L.n_pad * 8 : 0), 256);
   L.stats_off = off;
   off = align_up(off + (size_t)NSLOT * 8 * 8, 256);
   L.sched_off = off;
@@ -99,7 +104,7 @@ struct KernelArgs {
   uint64_t* grid;
   uint64_t* agent;
   uint32_t* episode;
-  uint32_t* balls;
+  uint64_t* balls;
   unsigned long long* stats;
   unsigned int* sched;  // persistent tile scheduler {next tile, CTAs done}
   const uint8_t* actions;

@@ -13,35 +13,42 @@ namespace navix {
 // Compile-time configuration of one kernel instantiation.
 template <int FAM, int H, int W>
 struct Cfg {
-  static constexpr int RS = 3;                       // KeyCorridor room size (W <= 8 -> 3)
+  static constexpr int RW = W > 8 ? 2 : 1;           // u64 planes per grid row (f2: 16-byte rows)
+  static constexpr int NPL = RW == 1 ? 8 : 32;       // SMEM planes per env (8 lines / 16 rows x 2)
+  static constexpr int RS = (W - 1) / 3 + 1;         // KeyCorridor room size (3 columns of rooms)
   static constexpr int NR = (H - 1) / (RS - 1);      // KeyCorridor rows
   static constexpr int T = FAM == FAM_DOORKEY ? 10 * W * W
                          : FAM == FAM_KEYCORRIDOR ? 30 * RS * RS
                          : 4 * W * H;                // R#16
   static constexpr int NA = FAM == FAM_DYNOBS ? 3 : 7;
-  static constexpr int NOBST = FAM != FAM_DYNOBS ? 0 : (W == 5 ? 2 : W == 6 ? 3 : 4);  // R#6
+  static constexpr int NOBST = FAM != FAM_DYNOBS ? 0 : (W == 5 ? 2 : W == 6 ? 3 : W == 16 ? 8 : 4);  // R#6
 };
 
-// Static layout row y as 8 cell bytes (bytes >= W are 0 = outside the grid).
+// Static layout plane p (row y = p / RW, cells x = 8 (p % RW) .. +7) as 8
+// cell bytes (cells x >= W are 0 = outside the grid).
 template <int FAM, int H, int W>
-__host__ __device__ constexpr uint64_t template_row(int y) {
+__host__ __device__ constexpr uint64_t template_plane(int p) {
+  constexpr int RW = W > 8 ? 2 : 1;
+  const int y = p / RW, x0 = 8 * (p % RW);
   uint64_t r = 0;
-  for (int x = 0; x < W; ++x) {
+  for (int x = x0; x < x0 + 8 && x < W; ++x) {
     bool wall;
     if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
     else wall = x == 0 || y == 0 || x == W - 1 || y == H - 1;
     uint8_t c = wall ? CELL_WALL : CELL_EMPTY;
     if (FAM != FAM_KEYCORRIDOR && x == W - 2 && y == H - 2) c = CELL_GOAL;  // goal (W-2, H-2)
-    r |= (uint64_t)c << (8 * x);
+    r |= (uint64_t)c << (8 * (x - x0));
   }
   return r;
 }
 
-// Per-thread view of its env's SMEM row lines: rows[y * TILE] is row y.
-struct RowView {
-  uint64_t* rows;  // &s_rows[0][tid]
+// Per-thread view of its env's SMEM rows: plane y * RW + x / 8 holds cells
+// x..x+7 of row y (stride TILE between planes).
+template <int RW>
+struct RowViewT {
+  uint64_t* rows;  // &planes[0][tid]
   __device__ __forceinline__ uint8_t* at(int x, int y) const {
-    return reinterpret_cast<uint8_t*>(rows + y * TILE) + x;
+    return reinterpret_cast<uint8_t*>(rows + (y * RW + (x >> 3)) * TILE) + (x & 7);
   }
   __device__ __forceinline__ uint8_t get(int x, int y) const { return *at(x, y); }
   __device__ __forceinline__ void set(int x, int y, uint8_t v) const { *at(x, y) = v; }
@@ -68,17 +75,31 @@ __device__ __forceinline__ int select64(uint64_t m, uint32_t k) {
 
 struct GenOut {
   int ax, ay, dir;
-  uint32_t balls;
+  uint64_t balls;  // DynObs: byte b = (x << 4) | y of ball b (up to 8)
   uint32_t fail;
 };
 
+// k-th set bit of a multi-word mask (word w covers bits 64w ..).
+template <int NW>
+__device__ __forceinline__ int select_bits(const uint64_t (&m)[NW], uint32_t k) {
+  int base = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t c = __popcll(m[w]);
+    if (k < c) return base + select64(m[w], k);
+    k -= c;
+    base += 64;
+  }
+  return -1;
+}
+
 template <int FAM, int H, int W>
-__device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t episode, uint32_t klo,
-                                              uint32_t khi) {
+__device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, uint32_t genv, uint32_t episode,
+                                              uint32_t klo, uint32_t khi) {
   using C = Cfg<FAM, H, W>;
   GenOut o{1, 1, 0, 0u, 0u};
 #pragma unroll
-  for (int y = 0; y < H; ++y) g.rows[y * TILE] = template_row<FAM, H, W>(y);
+  for (int p = 0; p < H * C::RW; ++p) g.rows[p * TILE] = template_plane<FAM, H, W>(p);
   DrawStream ds(genv, episode, 0u, klo, khi);
 
   if constexpr (FAM == FAM_DOORKEY) {
@@ -104,34 +125,41 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
       if (y != gy) g.set(gx, y, CELL_LAVA);
   } else if constexpr (FAM == FAM_DYNOBS) {
     // [MG] DynamicObstaclesEnv._gen_grid: balls uniform over empty cells, not the agent
-    uint64_t freem = 0;
+    // (free-cell bit y * 16 + x, row-major)
+    constexpr int NWD = (H * 16 + 63) / 64;
+    uint64_t freem[NWD];
+#pragma unroll
+    for (int w = 0; w < NWD; ++w) freem[w] = 0;
 #pragma unroll
     for (int y = 1; y <= H - 2; ++y)
 #pragma unroll
-      for (int x = 1; x <= W - 2; ++x) freem |= 1ull << (y * 8 + x);
-    freem &= ~(1ull << ((H - 2) * 8 + (W - 2)));  // goal
-    freem &= ~(1ull << (1 * 8 + 1));              // agent (1, 1)
+      for (int x = 1; x <= W - 2; ++x) freem[(y * 16 + x) >> 6] |= 1ull << ((y * 16 + x) & 63);
+    freem[((H - 2) * 16 + (W - 2)) >> 6] &= ~(1ull << (((H - 2) * 16 + (W - 2)) & 63));  // goal
+    freem[(1 * 16 + 1) >> 6] &= ~(1ull << ((1 * 16 + 1) & 63));                          // agent (1, 1)
 #pragma unroll
     for (int b = 0; b < C::NOBST; ++b) {
       const uint32_t u = ds.next();
-      const uint32_t cnt = __popcll(freem);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int w = 0; w < NWD; ++w) cnt += __popcll(freem[w]);
       if (cnt == 0) { o.fail += 1; continue; }
-      const int pos = select64(freem, bounded(u, cnt));
-      freem &= ~(1ull << pos);
-      const int x = pos & 7, y = pos >> 3;
+      const int pos = select_bits(freem, bounded(u, cnt));
+      freem[pos >> 6] &= ~(1ull << (pos & 63));
+      const int x = pos & 15, y = pos >> 4;
       g.set(x, y, make_cell(K_BALL, COL_BLUE));
-      o.balls |= (uint32_t)((x << 4) | y) << (8 * b);
+      o.balls |= (uint64_t)((x << 4) | y) << (8 * b);
     }
   } else if constexpr (FAM == FAM_KEYCORRIDOR) {
     // [MG] RoomGrid._gen_grid + KeyCorridorEnv._gen_grid + connect_all
     constexpr int S = C::RS, NR = C::NR, NC = 3, NROOM = NR * NC;
-    static_assert(S == 3, "grids <= 8x8 imply room size 3");
-    // door_pos[0].y / door_pos[1].x draws: _rand_int over a range of S-2 = 1
-    // value, so the positions are fixed, but the draws are consumed
+    // door_pos[0].y (right wall) and door_pos[1].x (bottom wall) per room,
+    // drawn room by room (j outer, i inner) as [MG] does
+    uint8_t dpy[NROOM], dpx[NROOM];
     for (int j = 0; j < NR; ++j)
       for (int i = 0; i < NC; ++i) {
-        if (i < NC - 1) (void)ds.next();
-        if (j < NR - 1) (void)ds.next();
+        const int r = j * NC + i;
+        if (i < NC - 1) dpy[r] = (uint8_t)(j * (S - 1) + 1 + ds.next_bounded(S - 2));
+        if (j < NR - 1) dpx[r] = (uint8_t)(i * (S - 1) + 1 + ds.next_bounded(S - 2));
       }
     // room links as bit masks over rooms r = 3j + i: H bit r = rooms r, r+1
     // linked; V bit r = rooms r, r+3 linked (removed walls and doors of any state)
@@ -145,24 +173,24 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
     const int room_idx = (int)ds.next_bounded(NR);
     const uint8_t door_col = (uint8_t)ds.next_bounded(6);           // R#23
     const int locked_room = room_idx * NC + 2;
-    g.set(2 * (S - 1), room_idx * (S - 1) + 1, make_cell(K_DOOR_LOCKED, door_col));
+    g.set(2 * (S - 1), dpy[room_idx * NC + 1], make_cell(K_DOOR_LOCKED, door_col));
     Hl |= 1u << (locked_room - 1);
     // object placement inside room (ri, rj): empty, not the default agent
     // cell, Manhattan distance >= 2 from it (reject_next_to, R#25)
     auto place_in_room = [&](int ri, int rj, uint8_t cell) {
       const uint32_t u = ds.next();
-      uint32_t m = 0;
+      uint64_t m = 0;
       int n = 0;
       for (int yy = 0; yy < S; ++yy)
         for (int xx = 0; xx < S; ++xx) {
           const int x = ri * (S - 1) + xx, y = rj * (S - 1) + yy;
           const int d = abs(x - adx) + abs(y - ady);
           const bool ok = x < W && y < H && g.get(x, y) == CELL_EMPTY && d >= 2;
-          m |= (ok ? 1u : 0u) << (yy * S + xx);
+          m |= (ok ? 1ull : 0ull) << (yy * S + xx);
           n += ok;
         }
       if (n == 0) { o.fail += 1; return; }
-      int p = select64(m, bounded(u, (uint32_t)n));
+      const int p = select64(m, bounded(u, (uint32_t)n));
       g.set(ri * (S - 1) + p % S, rj * (S - 1) + p / S, cell);
     };
     const uint8_t ball_col = (uint8_t)ds.next_bounded(6);
@@ -172,7 +200,10 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
     // place_agent(1, NR/2): (pos, dir) uniform over pairs whose front is empty or a wall
     {
       const uint32_t u = ds.next();
-      uint64_t m = 0;
+      constexpr int NWD = (S * S * 4 + 63) / 64;
+      uint64_t m[NWD];
+#pragma unroll
+      for (int w = 0; w < NWD; ++w) m[w] = 0;
       int n = 0;
       const int rx = S - 1, ry = (NR / 2) * (S - 1);
       for (int yy = 0; yy < S; ++yy)
@@ -183,14 +214,15 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
             const int fx = x + (d == 0) - (d == 2), fy = y + (d == 1) - (d == 3);
             const uint8_t f = g.get(fx, fy);
             const bool ok = f == CELL_EMPTY || (f & 15) == K_WALL;
-            m |= (ok ? 1ull : 0ull) << ((yy * S + xx) * 4 + d);
+            const int bit = (yy * S + xx) * 4 + d;
+            m[bit >> 6] |= (ok ? 1ull : 0ull) << (bit & 63);
             n += ok;
           }
         }
       if (n == 0) {
         o.fail += 1;
       } else {
-        const int p = select64(m, bounded(u, (uint32_t)n));
+        const int p = select_bits(m, bounded(u, (uint32_t)n));
         o.dir = p & 3;
         o.ax = rx + (p >> 2) % S;
         o.ay = ry + (p >> 2) / S;
@@ -218,15 +250,14 @@ __device__ __noinline__ GenOut generate_level(RowView g, uint32_t genv, uint32_t
       const bool has = k == 0 ? i < NC - 1 : k == 1 ? j < NR - 1 : k == 2 ? i > 0 : j > 0;
       if (!has) continue;
       const int nb = k == 0 ? r + 1 : k == 1 ? r + NC : k == 2 ? r - 1 : r - NC;
-      const int lo = r < nb ? r : nb;  // link bit: the lower room of the pair
+      const int lo = r < nb ? r : nb;  // the link's lower room: its door_pos[0] or door_pos[1]
       const bool horiz = (k & 1) == 0;
       if ((((horiz ? Hl : Vl) >> lo) & 1u)) continue;
       if (r == locked_room || nb == locked_room) continue;
       const uint8_t col = (uint8_t)ds.next_bounded(6);
-      // door_pos[k] of room (i, j) with room size 3
       const int li = lo % NC, lj = lo / NC;
-      const int x = horiz ? li * (S - 1) + S - 1 : li * (S - 1) + 1;
-      const int y = horiz ? lj * (S - 1) + 1 : lj * (S - 1) + S - 1;
+      const int x = horiz ? li * (S - 1) + S - 1 : dpx[lo];
+      const int y = horiz ? dpy[lo] : lj * (S - 1) + S - 1;
       g.set(x, y, make_cell(K_DOOR_CLOSED, col));
       if (horiz) Hl |= 1u << lo;
       else Vl |= 1u << lo;

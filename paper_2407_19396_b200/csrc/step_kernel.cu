@@ -112,29 +112,31 @@ __device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) 
 // per-lane SMEM word stride 147 is odd: bank-conflict free).
 
 // One tile's input buffers in SMEM (filled by TMA bulk copies).
-template <int FAM>
+template <int FAM, int NPL>
 struct TileSmem {
-  uint64_t rows[8][TILE];                            // grid rows; later this env's view lines
+  uint64_t rows[NPL][TILE];                          // grid row planes; later this env's view lines
   uint64_t agent[TILE];                              // agent records
-  uint32_t balls[FAM == FAM_DYNOBS ? TILE : 4];      // DynObs ball positions
+  uint64_t balls[FAM == FAM_DYNOBS ? TILE : 2];      // DynObs ball positions
   uint32_t episode[FAM == FAM_DYNOBS ? TILE : 4];    // DynObs episode counters
   uint8_t act[TILE];                                 // actions (env order)
 };
 
 // Thread 0: bulk-copy tile `tile`'s inputs into `b`, completing on `mbar`.
 // Returns whether the actions came along (full tile, 16-B aligned base).
-template <int FAM, int H, int MODE>
-__device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t tile, TileSmem<FAM>& b, uint32_t mbar) {
+template <int FAM, int HP, int MODE, int NPL>
+__device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t tile, TileSmem<FAM, NPL>& b,
+                                                 uint32_t mbar) {
+  // HP = grid planes per env (H rows x RW u64)
   const int64_t tile0 = tile * TILE;
   const bool act_bulk = MODE == MODE_STEP && a.bulk_act && tile0 + TILE <= a.n;
-  const uint32_t bytes = H * TILE * 8 + TILE * 8 + (act_bulk ? TILE : 0) +
-                         (FAM == FAM_DYNOBS ? (MODE == MODE_STEP ? 8 : 4) * TILE : 0);
+  const uint32_t bytes = HP * TILE * 8 + TILE * 8 + (act_bulk ? TILE : 0) +
+                         (FAM == FAM_DYNOBS ? (MODE == MODE_STEP ? 12 : 8) * TILE : 0);
   mbar_expect_tx(mbar, bytes);
-  bulk_g2s(&b.rows[0][0], a.grid + tile0 * H, H * TILE * 8, mbar);
+  bulk_g2s(&b.rows[0][0], a.grid + tile0 * HP, HP * TILE * 8, mbar);
   bulk_g2s(b.agent, a.agent + tile0, TILE * 8, mbar);
   if (act_bulk) bulk_g2s(b.act, a.actions + tile0, TILE, mbar);
   if (FAM == FAM_DYNOBS) {
-    bulk_g2s(b.balls, a.balls + tile0, TILE * 4, mbar);
+    bulk_g2s(b.balls, a.balls + tile0, TILE * 8, mbar);
     if (MODE == MODE_STEP) bulk_g2s(b.episode, a.episode + tile0, TILE * 4, mbar);
   }
   return act_bulk;
@@ -147,8 +149,8 @@ __device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t ti
 struct EnvResult {
   float reward;
   bool valid, regen, term, trunc, dirty;
-  uint64_t nrec;
-  uint32_t episode, balls;
+  uint64_t nrec, balls;
+  uint32_t episode;
   uint32_t st[8];
 };
 
@@ -157,13 +159,13 @@ struct EnvResult {
 struct EnvIn {
   uint64_t rec;      // agent record
   uint32_t act;      // action
-  uint32_t balls;    // DynObs ball positions
+  uint64_t balls;    // DynObs ball positions (byte b = (x << 4) | y)
   uint32_t episode;  // episode counter
   bool episode_known;  // else read from HBM when an auto-reset needs it
 };
 
-template <int FAM, int MODE>
-__device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile, const TileSmem<FAM>& b) {
+template <int FAM, int MODE, int NPL>
+__device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile, const TileSmem<FAM, NPL>& b) {
   const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
   const int64_t tile0 = tile * TILE, e = tile0 + le;
   EnvIn in{0, 0, 0, 0, false};
@@ -201,12 +203,14 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   const int64_t e = tile0 + le;       // env index (caller arrays)
   const bool valid = e < a.n;
   const uint32_t genv = a.env_begin + (uint32_t)e;  // global env index: Philox counter word c0
-  RowView g{rows};
+  constexpr int RW = C::RW;
+  RowViewT<RW> g{rows};
 
   // ---- a1: inputs
   uint8_t act = (uint8_t)in.act;
   const uint64_t rec = in.rec;
-  uint32_t balls = in.balls, episode = in.episode;
+  uint64_t balls = in.balls;
+  uint32_t episode = in.episode;
   int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
   uint8_t carry = (uint8_t)(rec >> 24);
   uint32_t sc = (uint32_t)((rec >> 32) & 0xFFFF);
@@ -227,7 +231,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     __shared__ int s_qn;
     __shared__ int s_q[TILE];
     __shared__ uint32_t s_qep[TILE];
-    __shared__ uint64_t s_qout[TILE];
+    __shared__ uint32_t s_qout[TILE];
+    __shared__ uint64_t s_qballs[TILE];
     if (tid == 0) s_qn = 0;
     __syncthreads();
     if (regen) {
@@ -239,17 +244,18 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     for (int q = tid; q < nq; q += TILE) {
       const int st = s_q[q];
       const uint32_t genv_t = a.env_begin + (uint32_t)(tile0 + env_of_slot(st));
-      const GenOut o = generate_level<FAM, H, W>(RowView{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi);
-      s_qout[st] = (uint64_t)o.balls | ((uint64_t)o.ax << 32) | ((uint64_t)o.ay << 40) | ((uint64_t)o.dir << 48) |
-                   ((uint64_t)o.fail << 56);
+      const GenOut o =
+          generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi);
+      s_qballs[st] = o.balls;
+      s_qout[st] = (uint32_t)o.ax | ((uint32_t)o.ay << 8) | ((uint32_t)o.dir << 16) | (o.fail << 24);
     }
     __syncthreads();
     if (regen) {
-      const uint64_t o = s_qout[tid];
+      const uint32_t o = s_qout[tid];
       episode = s_qep[tid];
-      balls = (uint32_t)o;
-      ax = (int)((o >> 32) & 0xFF); ay = (int)((o >> 40) & 0xFF); dir = (int)((o >> 48) & 3);
-      st_fail = (uint32_t)(o >> 56);
+      balls = s_qballs[tid];
+      ax = (int)(o & 0xFF); ay = (int)((o >> 8) & 0xFF); dir = (int)((o >> 16) & 3);
+      st_fail = o >> 24;
       carry = CELL_EMPTY;
       sc = 0;
       prev_done = false;
@@ -274,7 +280,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     if (FAM == FAM_DYNOBS) {
 #pragma unroll
       for (int bb = 0; bb < C::NOBST; ++bb) {
-        const uint32_t p = (balls >> (8 * bb)) & 0xFF;
+        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
         if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
       }
     }
@@ -288,28 +294,40 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         if (act >= 3) act = 0;
         const uint8_t f0 = g.get(fx, fy);
         not_clear = f0 != CELL_EMPTY && (f0 & 15) != K_GOAL;
-        const uint4 u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
+        // one Philox block per 4 balls: (env, episode, 1 << 16 | step, block)
+        uint4 u = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int bb = 0; bb < C::NOBST; ++bb) {
-          const uint32_t p = (balls >> (8 * bb)) & 0xFF;
+          if ((bb & 3) == 0)
+            u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, (uint32_t)(bb >> 2)), a.key_lo, a.key_hi);
+          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
           if (!p) continue;
           const int bx = p >> 4, by = p & 15;
           // admissible cells of the 3x3 box, row-major bit k = 4*dy + dx: empty
-          // (cell byte == 0x01: a byte permute gathers the 3 cells of each
-          // row, a SWAR exact-zero test finds the empty ones) and not the agent
-          const uint32_t sel = (uint32_t)((bx - 1) | (bx << 4) | ((bx + 1) << 8));
+          // (cell byte == 0x01) and not the agent
           uint32_t m = 0;
+          if constexpr (RW == 1) {
+            // a byte permute gathers the 3 cells of each row, a SWAR exact-zero
+            // test finds the empty ones
+            const uint32_t sel = (uint32_t)((bx - 1) | (bx << 4) | ((bx + 1) << 8));
 #pragma unroll
-          for (int dy = 0; dy < 3; ++dy) {
-            const uint64_t line = rows[(by - 1 + dy) * TILE];
-            const uint32_t x = prmt((uint32_t)line, (uint32_t)(line >> 32), sel) ^ 0x01010101u;
-            const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // bit 7: byte == 0
-            m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (4 * dy);
+            for (int dy = 0; dy < 3; ++dy) {
+              const uint64_t line = rows[(by - 1 + dy) * TILE];
+              const uint32_t x = prmt((uint32_t)line, (uint32_t)(line >> 32), sel) ^ 0x01010101u;
+              const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // bit 7: byte == 0
+              m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (4 * dy);
+            }
+          } else {
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+                m |= (g.get(bx - 1 + dx, by - 1 + dy) == CELL_EMPTY ? 1u : 0u) << (4 * dy + dx);
           }
           const int adx = ax - (bx - 1), ady = ay - (by - 1);
           if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (4 * ady + adx));
           if (m) {
-            const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
+            const uint32_t ub = (bb & 3) == 0 ? u.x : (bb & 3) == 1 ? u.y : (bb & 3) == 2 ? u.z : u.w;
             uint32_t kk = bounded(ub, __popc(m)), k = 0;  // kk-th set bit (row-major order)
             uint32_t c = __popc(m & 0xFFu);
             if (kk >= c) { kk -= c; k = 8; }
@@ -323,7 +341,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
             const int nx = bx - 1 + (int)(k & 3), ny = by - 1 + (int)(k >> 2);
             g.set(nx, ny, make_cell(K_BALL, COL_BLUE));
             g.set(bx, by, CELL_EMPTY);
-            balls = (balls & ~(0xFFu << (8 * bb))) | ((uint32_t)((nx << 4) | ny) << (8 * bb));
+            balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)((nx << 4) | ny) << (8 * bb));
           }
         }
       }
@@ -386,15 +404,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 
   // ---- a7a: grid write-back (only when modified), before the lines are reused
   if (MODE != MODE_OBSERVE && grid_dirty && scratch == nullptr) {
-    uint64_t* gdst = a.grid + tile0 * H + tid;
+    uint64_t* gdst = a.grid + tile0 * H * RW + tid;
 #pragma unroll
-    for (int y = 0; y < H; ++y)
-      gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : rows[y * TILE];
+    for (int p = 0; p < H * RW; ++p)
+      gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : rows[p * TILE];
   }
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
   const uint64_t* lines = rows;
-  if (dir & 1) {
+  if (RW == 1 && (dir & 1)) {
     if (scratch) {
 #pragma unroll
       for (int y = 0; y < 8; ++y) scratch[y * TILE] = rows[y * TILE];
@@ -408,7 +426,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
-    observe_emit(lines, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
+    if constexpr (RW == 1) observe_emit(lines, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
+    else observe_emit_wide(rows, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
 
   EnvResult r;
@@ -485,25 +504,33 @@ __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, co
 // ------------------------------------------------------------------ kernels
 // One tile per CTA (reset, observe; step when NAVIX_STEP_KERNEL=onetile).
 // 28 KB of SMEM: up to 8 CTAs per SM with <= 64 registers.
+template <int FAM, int NPL>
+struct OneTileSmem {
+  uint8_t obs[TILE * OBS_BYTES];
+  TileSmem<FAM, NPL> buf;
+  uint64_t scratch[NPL == 8 ? 8 : 1][TILE];  // rollout: column view of odd directions (narrow grids)
+  uint64_t mbar;
+};
+extern __shared__ __align__(128) uint8_t navix_dyn_smem[];
+
 template <int FAM, int H, int W, int MODE>
-__global__ void __launch_bounds__(TILE, 8) navix_kernel(const KernelArgs a) {
-  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
-  __shared__ __align__(128) TileSmem<FAM> s_buf;
-  __shared__ __align__(8) uint64_t s_mbar;
+__global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const KernelArgs a) {
+  using C = Cfg<FAM, H, W>;
+  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL>*>(navix_dyn_smem);
   if (MODE != MODE_RESET) {
-    const uint32_t mbar = smem_u32(&s_mbar);
+    const uint32_t mbar = smem_u32(&S.mbar);
     if (threadIdx.x == 0) {
       mbar_init(mbar, 1);
-      issue_tile_loads<FAM, H, MODE>(a, blockIdx.x, s_buf, mbar);
+      issue_tile_loads<FAM, H * C::RW, MODE>(a, blockIdx.x, S.buf, mbar);
     }
     __syncthreads();  // mbarrier initialised before anyone waits on it
     mbar_wait(mbar, 0);
   }
-  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, &s_buf.rows[0][threadIdx.x], nullptr,
-                                                    decode_staged<FAM, MODE>(a, blockIdx.x, s_buf), s_obs, [] {});
+  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, &S.buf.rows[0][threadIdx.x], nullptr,
+                                                    decode_staged<FAM, MODE>(a, blockIdx.x, S.buf), S.obs, [] {});
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  store_obs(a, blockIdx.x, s_obs, threadIdx.x, TILE, threadIdx.x == 0);
+  store_obs(a, blockIdx.x, S.obs, threadIdx.x, TILE, threadIdx.x == 0);
   tile_store<FAM, MODE>(a, blockIdx.x, r);
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -521,7 +548,8 @@ __global__ void __launch_bounds__(TILE, 8) navix_kernel(const KernelArgs a) {
 template <int FAM, int H, int W>
 __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
   __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
-  __shared__ __align__(128) TileSmem<FAM> s_buf[2];
+  using C = Cfg<FAM, H, W>;
+  __shared__ __align__(128) TileSmem<FAM, C::NPL> s_buf[2];
   __shared__ __align__(8) uint64_t s_mbar[2];   // tile inputs landed (per buffer)
   __shared__ int64_t s_tile[2];
   const int64_t n_tiles = (a.n + TILE - 1) / TILE;
@@ -532,7 +560,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   // s_mbar[k] always publishes s_tile[k].
   auto publish = [&](int k, int64_t t) {
     s_tile[k] = t;
-    if (t < n_tiles) issue_tile_loads<FAM, H, MODE_STEP>(a, t, s_buf[k], smem_u32(&s_mbar[k]));
+    if (t < n_tiles) issue_tile_loads<FAM, H * C::RW, MODE_STEP>(a, t, s_buf[k], smem_u32(&s_mbar[k]));
     else mbar_arrive(smem_u32(&s_mbar[k]));
   };
   if (tid == 0) {
@@ -580,21 +608,23 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
 // navix_step calls; outputs of step t at [t][n].
 template <int FAM, int H, int W>
 __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a, int64_t K) {
-  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
-  __shared__ __align__(128) TileSmem<FAM> s_buf;
-  __shared__ __align__(16) uint64_t s_scratch[8][TILE];
-  __shared__ __align__(8) uint64_t s_mbar;
+  using C = Cfg<FAM, H, W>;
+  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL>*>(navix_dyn_smem);
+  uint8_t* const s_obs = S.obs;
+  auto& s_buf = S.buf;
+  auto& s_scratch = S.scratch;
+  auto& s_mbar = S.mbar;
   const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
   const int64_t tile = blockIdx.x, tile0 = tile * TILE, slot = tile0 + tid, e = tile0 + le;
   const bool valid = e < a.n;
   const uint32_t mbar = smem_u32(&s_mbar);
   if (tid == 0) {
     mbar_init(mbar, 1);
-    issue_tile_loads<FAM, H, MODE_OBSERVE>(a, tile, s_buf, mbar);  // rows, agents (+ balls)
+    issue_tile_loads<FAM, H * C::RW, MODE_OBSERVE>(a, tile, s_buf, mbar);  // rows, agents (+ balls)
   }
   __syncthreads();
   mbar_wait(mbar, 0);
-  EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0u, a.episode[slot], true};
+  EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
   bool dirty = false;
   uint32_t next_act = valid ? a.actions[e] : 0u;
   for (int64_t t = 0; t < K; ++t) {
@@ -606,7 +636,8 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     as.terminated = a.terminated + t * a.n;
     as.truncated = a.truncated + t * a.n;
     as.bulk_obs = (reinterpret_cast<uintptr_t>(as.obs) & 15u) == 0;
-    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(as, tile, &s_buf.rows[0][tid], &s_scratch[0][tid], in,
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(as, tile, &s_buf.rows[0][tid],
+                                                           C::RW == 1 ? &s_scratch[0][tid] : nullptr, in,
                                                            s_obs, [&] {
       if (t > 0) {  // the previous step's store must have read s_obs
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -628,10 +659,10 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     if (FAM == FAM_DYNOBS) a.balls[slot] = in.balls;
   }
   if (dirty) {
-    uint64_t* gdst = a.grid + tile0 * H + tid;
+    uint64_t* gdst = a.grid + tile0 * H * C::RW + tid;
 #pragma unroll
-    for (int y = 0; y < H; ++y)
-      gdst[y * TILE] = FAM == FAM_DYNOBS ? template_row<FAM, H, W>(y) : s_buf.rows[y][tid];
+    for (int p = 0; p < H * C::RW; ++p)
+      gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : s_buf.rows[p][tid];
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -642,43 +673,50 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
 // path: one thread per env, staged in SMEM, coalesced copy-out.
 template <int FAM, int H, int W>
 __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint8_t* out) {
-  constexpr int PER = 3 * W * H;
-  __shared__ __align__(16) uint8_t s_out[TILE * PER];
+  constexpr int PER = 3 * W * H, RW = row_planes(W);
+  constexpr bool STAGE = TILE * PER <= 32 * 1024;  // small grids: SMEM staging + coalesced copy-out
+  __shared__ __align__(16) uint8_t s_out[STAGE ? TILE * PER : 16];
   const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
   const int64_t tile0 = (int64_t)blockIdx.x * TILE, slot = tile0 + tid;
+  const int64_t nv = a.n - tile0;
+  const int nvalid = nv >= TILE ? TILE : (int)nv;
   const uint64_t rec = a.agent[slot];
-  uint64_t rows[H];
+  uint64_t pl[H * RW];
 #pragma unroll
-  for (int y = 0; y < H; ++y) rows[y] = a.grid[tile0 * H + y * TILE + tid];
+  for (int p = 0; p < H * RW; ++p) pl[p] = a.grid[tile0 * H * RW + p * TILE + tid];
   if (FAM == FAM_DYNOBS) {
-    const uint32_t bl = a.balls[slot];
+    const uint64_t bl = a.balls[slot];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t p = (bl >> (8 * b)) & 0xFF;
+    for (int b = 0; b < Cfg<FAM, H, W>::NOBST; ++b) {
+      const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
+      const int bx = q >> 4, by = q & 15;
 #pragma unroll
-      for (int y = 0; y < H; ++y)
-        if (p && (int)(p & 15) == y)
-          rows[y] = (rows[y] & ~(0xFFull << (8 * (p >> 4)))) | ((uint64_t)make_cell(K_BALL, COL_BLUE) << (8 * (p >> 4)));
+      for (int p = 0; p < H * RW; ++p)
+        if (q && p == by * RW + (bx >> 3))
+          pl[p] = (pl[p] & ~(0xFFull << (8 * (bx & 7)))) | ((uint64_t)make_cell(K_BALL, COL_BLUE) << (8 * (bx & 7)));
     }
   }
   const int ax = (int)(rec & 0xFF), ay = (int)((rec >> 8) & 0xFF), dir = (int)((rec >> 16) & 3);
-  uint8_t* o = s_out + le * PER;
+  uint8_t* o = STAGE ? s_out + le * PER : out + (tile0 + le) * PER;
+  const bool write = STAGE || le < nvalid;
 #pragma unroll
   for (int y = 0; y < H; ++y)
 #pragma unroll
     for (int x = 0; x < W; ++x) {
-      const uint32_t c = (uint32_t)(rows[y] >> (8 * x)) & 0xFF, kind = c & 15;
-      uint8_t* t = o + (x * H + y) * 3;
+      const uint32_t c = (uint32_t)(pl[y * RW + (x >> 3)] >> (8 * (x & 7))) & 0xFF, kind = c & 15;
       const bool ag = x == ax && y == ay;
-      t[0] = ag ? 10 : (kind >= 11 ? 4 : kind);
-      t[1] = ag ? 0 : (c >> 4) & 7;
-      t[2] = ag ? dir : (kind >= 11 ? kind - 10 : 0);
+      if (write) {
+        uint8_t* t = o + (x * H + y) * 3;
+        t[0] = ag ? 10 : (kind >= 11 ? 4 : kind);
+        t[1] = ag ? 0 : (c >> 4) & 7;
+        t[2] = ag ? dir : (kind >= 11 ? kind - 10 : 0);
+      }
     }
-  __syncthreads();
-  const int64_t nv = a.n - tile0;
-  const int nvalid = nv >= TILE ? TILE : (int)nv;
-  uint8_t* dst = out + tile0 * PER;
-  for (int i = tid; i < nvalid * PER; i += TILE) dst[i] = s_out[i];
+  if (STAGE) {
+    __syncthreads();
+    uint8_t* dst = out + tile0 * PER;
+    for (int i = tid; i < nvalid * PER; i += TILE) dst[i] = s_out[i];
+  }
 }
 
 // ------------------------------------------------------------------ other kernels
@@ -707,37 +745,54 @@ __global__ void stats_reduce_kernel(const unsigned long long* slots, long long* 
 }
 
 // ------------------------------------------------------------------ dispatch
+template <class K>
+static void allow_dyn_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 template <int FAM, int H, int W>
 static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
   const dim3 block(TILE);
+  using C = Cfg<FAM, H, W>;
+  constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL>);
+  static bool attrs = false;
+  if (!attrs) {
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_STEP>, DYN);
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_RESET>, DYN);
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_OBSERVE>, DYN);
+    allow_dyn_smem(navix_rollout_kernel<FAM, H, W>, DYN);
+    attrs = true;
+  }
   static int onetile = -1;
   if (onetile < 0) {
     const char* v = getenv("NAVIX_STEP_KERNEL");  // experiment switch
     onetile = v && v[0] == 'o';
   }
-  if (mode == MODE_STEP && onetile) {
-    navix_kernel<FAM, H, W, MODE_STEP><<<(unsigned)n_tiles, block, 0, s>>>(a);
+  if (mode == MODE_STEP && (onetile || W > 8)) {  // wide grids: one tile per CTA (SMEM)
+    navix_kernel<FAM, H, W, MODE_STEP><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   } else if (mode == MODE_STEP) {
-    // persistent grid: as many CTAs as fit on the device at once
-    static int per_sm = -1, n_sm = -1;
-    if (per_sm < 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W>, TILE, 0);
-      if (per_sm < 1) per_sm = 1;
+    if constexpr (W <= 8) {
+      // persistent grid: as many CTAs as fit on the device at once
+      static int per_sm = -1, n_sm = -1;
+      if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W>, TILE, 0);
+        if (per_sm < 1) per_sm = 1;
+      }
+      const int64_t cap = (int64_t)per_sm * n_sm;
+      const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
+      navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
     }
-    const int64_t cap = (int64_t)per_sm * n_sm;
-    const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
-    navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
   } else if (mode == MODE_FULL_OBS) {
     full_obs_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
   } else if (mode == MODE_ROLLOUT) {
-    navix_rollout_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.rollout_steps);
+    navix_rollout_kernel<FAM, H, W><<<(unsigned)n_tiles, block, DYN, s>>>(a, a.rollout_steps);
   } else if (mode == MODE_RESET) {
-    navix_kernel<FAM, H, W, MODE_RESET><<<(unsigned)n_tiles, block, 0, s>>>(a);
+    navix_kernel<FAM, H, W, MODE_RESET><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   } else {
-    navix_kernel<FAM, H, W, MODE_OBSERVE><<<(unsigned)n_tiles, block, 0, s>>>(a);
+    navix_kernel<FAM, H, W, MODE_OBSERVE><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   }
   return cudaPeekAtLastError();
 }
@@ -760,6 +815,13 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
     case FAM_KEYCORRIDOR * 10000 + 307: return launch_fhw<FAM_KEYCORRIDOR, 3, 7>(mode, a, n_tiles, s);
     case FAM_KEYCORRIDOR * 10000 + 507: return launch_fhw<FAM_KEYCORRIDOR, 5, 7>(mode, a, n_tiles, s);
     case FAM_KEYCORRIDOR * 10000 + 707: return launch_fhw<FAM_KEYCORRIDOR, 7, 7>(mode, a, n_tiles, s);
+    // row f2: grids up to 16x16
+    case FAM_EMPTY * 10000 + 1616: return launch_fhw<FAM_EMPTY, 16, 16>(mode, a, n_tiles, s);
+    case FAM_DOORKEY * 10000 + 1616: return launch_fhw<FAM_DOORKEY, 16, 16>(mode, a, n_tiles, s);
+    case FAM_DYNOBS * 10000 + 1616: return launch_fhw<FAM_DYNOBS, 16, 16>(mode, a, n_tiles, s);
+    case FAM_KEYCORRIDOR * 10000 + 1010: return launch_fhw<FAM_KEYCORRIDOR, 10, 10>(mode, a, n_tiles, s);
+    case FAM_KEYCORRIDOR * 10000 + 1313: return launch_fhw<FAM_KEYCORRIDOR, 13, 13>(mode, a, n_tiles, s);
+    case FAM_KEYCORRIDOR * 10000 + 1616: return launch_fhw<FAM_KEYCORRIDOR, 16, 16>(mode, a, n_tiles, s);
     default: return cudaErrorInvalidConfiguration;
   }
 }

@@ -38,17 +38,16 @@ def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     assert (o.height, o.width, o.max_steps, o.n_actions, o.export_bytes) == (h, w, T, na, s.export_bytes)
 
 
-def test_unknown_and_unsupported_ids():
-    from paper_2407_19396_b200 import NavixError, load_library, spec_of
+def test_unknown_ids_and_row_f2_sizes():
+    from paper_2407_19396_b200 import NavixError, spec_of
     with pytest.raises(NavixError) as e:
         spec_of("Navix-NoSuchEnv-v0")
     assert e.value.status == 1 and "unknown env id" in str(e.value)
-    s = spec_of("Navix-DoorKey-16x16-v0")  # Table 9 id without a kernel yet: spec still known
-    assert (s.height, s.width, s.max_steps) == (16, 16, 2560)
-    lib = load_library()
-    h = ctypes.c_void_p()
-    assert lib.navix_create_shard(b"DoorKey-16x16", 8, 0, 8, 0, 0, None, 0, ctypes.byref(h)) == 5
-    assert b"no kernel" in lib.navix_last_error()
+    for env_id, hw, T, nob in (("Navix-DoorKey-16x16-v0", 16, 2560, 0), ("Navix-Empty-16x16-v0", 16, 1024, 0),
+                               ("Navix-Dynamic-Obstacles-16x16", 16, 1024, 8), ("KeyCorridorS4R3", 10, 480, 0),
+                               ("KeyCorridorS5R3", 13, 750, 0), ("Navix-KeyCorridorS6R3-v0", 16, 1080, 0)):
+        s = spec_of(env_id)  # row f2: grids up to 16x16 have kernels
+        assert (s.height, s.width, s.max_steps, s.n_obstacles) == (hw, hw, T, nob), env_id
 
 
 def test_argument_validation_before_any_cuda_call():

@@ -97,6 +97,13 @@ def test_parity_other_sizes_ragged(env_id):
     run_parity(env_id, 333, 400, block=333, seed=5)
 
 
+@pytest.mark.parametrize("env_id", ["Empty-16x16-v0", "DoorKey-16x16-v0", "Dynamic-Obstacles-16x16-v0",
+                                    "KeyCorridorS4R3-v0", "KeyCorridorS5R3-v0", "KeyCorridorS6R3-v0"])
+def test_parity_row_f2_wide_grids(env_id):
+    # grids up to 16x16 (16-byte rows, one tile per CTA): 4 full tiles + a ragged tail
+    run_parity(env_id, 555, 500, block=555, seed=12)
+
+
 @pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "LavaGapS7-v0", "Dynamic-Obstacles-8x8-v0"])
 def test_parity_reward_mode_navix(env_id):
     run_parity(env_id, 512, 300, block=512, reward_mode=1, seed=9)
