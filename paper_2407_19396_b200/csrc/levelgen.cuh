@@ -125,17 +125,17 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       if (y != gy) g.set(gx, y, CELL_LAVA);
   } else if constexpr (FAM == FAM_DYNOBS) {
     // [MG] DynamicObstaclesEnv._gen_grid: balls uniform over empty cells, not the agent
-    // (free-cell bit y * 16 + x, row-major)
-    constexpr int NWD = (H * 16 + 63) / 64;
+    // (free-cell bit y * RS + x, row-major; RS = 8 up to width 8: one word)
+    constexpr int RSB = W > 8 ? 16 : 8, NWD = (H * RSB + 63) / 64;
     uint64_t freem[NWD];
 #pragma unroll
     for (int w = 0; w < NWD; ++w) freem[w] = 0;
 #pragma unroll
     for (int y = 1; y <= H - 2; ++y)
 #pragma unroll
-      for (int x = 1; x <= W - 2; ++x) freem[(y * 16 + x) >> 6] |= 1ull << ((y * 16 + x) & 63);
-    freem[((H - 2) * 16 + (W - 2)) >> 6] &= ~(1ull << (((H - 2) * 16 + (W - 2)) & 63));  // goal
-    freem[(1 * 16 + 1) >> 6] &= ~(1ull << ((1 * 16 + 1) & 63));                          // agent (1, 1)
+      for (int x = 1; x <= W - 2; ++x) freem[(y * RSB + x) >> 6] |= 1ull << ((y * RSB + x) & 63);
+    freem[((H - 2) * RSB + (W - 2)) >> 6] &= ~(1ull << (((H - 2) * RSB + (W - 2)) & 63));  // goal
+    freem[(1 * RSB + 1) >> 6] &= ~(1ull << ((1 * RSB + 1) & 63));                           // agent (1, 1)
 #pragma unroll
     for (int b = 0; b < C::NOBST; ++b) {
       const uint32_t u = ds.next();
@@ -144,8 +144,13 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       for (int w = 0; w < NWD; ++w) cnt += __popcll(freem[w]);
       if (cnt == 0) { o.fail += 1; continue; }
       const int pos = select_bits(freem, bounded(u, cnt));
-      freem[pos >> 6] &= ~(1ull << (pos & 63));
-      const int x = pos & 15, y = pos >> 4;
+      if constexpr (NWD == 1) freem[0] &= ~(1ull << pos);
+      else {
+#pragma unroll
+        for (int w = 0; w < NWD; ++w)
+          if (w == (pos >> 6)) freem[w] &= ~(1ull << (pos & 63));
+      }
+      const int x = pos % RSB, y = pos / RSB;
       g.set(x, y, make_cell(K_BALL, COL_BLUE));
       o.balls |= (uint64_t)((x << 4) | y) << (8 * b);
     }

@@ -28,6 +28,10 @@ CONFIGS = [  # (env id, largest N) per BASELINE.json configs
     ("Dynamic-Obstacles-8x8-v0", 1 << 20),
     ("KeyCorridorS3R3-v0", 1 << 20),
     ("LavaGapS7-v0", 1 << 20),
+    ("Empty-16x16-v0", 1 << 20),
+    ("DoorKey-16x16-v0", 1 << 20),
+    ("Dynamic-Obstacles-16x16-v0", 1 << 20),
+    ("KeyCorridorS6R3-v0", 1 << 20),
 ]
 SIZES = [1, 8, 1 << 10, 1 << 11, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 21, 1 << 22, 1 << 23]
 
@@ -67,10 +71,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "sweep.json"))
+    ap.add_argument("--sizes", default="", help="comma-separated batch sizes (default: the full list)")
+    ap.add_argument("--envs", default="", help="comma-separated env ids (default: all)")
     a = ap.parse_args()
     rows = []
+    sizes = [int(x) for x in a.sizes.split(",") if x] or SIZES
+    envs = set(x for x in a.envs.split(",") if x)
     for env_id, nmax in CONFIGS:
-        for n in SIZES:
+        if envs and env_id not in envs:
+            continue
+        for n in sizes:
             if n > nmax:
                 continue
             r = time_point(env_id, n, a.steps)
