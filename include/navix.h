@@ -60,7 +60,9 @@ enum {
   NAVIX_FAMILY_DOORKEY = 1,
   NAVIX_FAMILY_DYNOBS = 2,
   NAVIX_FAMILY_KEYCORRIDOR = 3,
-  NAVIX_FAMILY_LAVAGAP = 4
+  NAVIX_FAMILY_LAVAGAP = 4,
+  NAVIX_FAMILY_EMPTY_RANDOM = 5,
+  NAVIX_FAMILY_DISTSHIFT = 6
 };
 
 /* Reward modes (R#1/R#3): MINIGRID = legacy 1 - 0.9*sc/T on success,

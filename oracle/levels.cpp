@@ -92,6 +92,34 @@ static void gen_empty(Env& e) {
   e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
 }
 
+// [MG] EmptyEnv._gen_grid with agent_start_pos=None: place_agent() over the
+// whole grid (empty cells, the goal excluded), then a random direction.
+static void gen_empty_random(Env& e, DrawStream& ds) {
+  int W = e.spec.width, H = e.spec.height;
+  e.grid = Grid(W, H);
+  e.grid.wall_rect(0, 0, W, H);
+  e.grid.set(W - 2, H - 2, make_goal());
+  e.agent_x = -1; e.agent_y = -1;
+  int ax, ay;
+  place_uniform(e, 0, 0, W, H, ds.next(), nullptr, &ax, &ay);
+  e.agent_x = ax; e.agent_y = ay;
+  e.agent_dir = (int)ds.next_bounded(4);
+}
+
+// [MG] DistShiftEnv._gen_grid: goal (width-2, 1), two lava strips of width-6
+// cells from x = 3 on rows 1 and strip2_row, agent (1,1) east.  No draws.
+static void gen_distshift(Env& e) {
+  int W = e.spec.width, H = e.spec.height;
+  e.grid = Grid(W, H);
+  e.grid.wall_rect(0, 0, W, H);
+  e.grid.set(W - 2, 1, make_goal());
+  for (int i = 0; i < W - 6; ++i) {
+    e.grid.set(3 + i, 1, make_lava());
+    e.grid.set(3 + i, e.spec.strip2_row, make_lava());
+  }
+  e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
+}
+
 // ---------------------------------------------------------------- DoorKey
 // [MG] DoorKeyEnv._gen_grid (SURVEY §8c-4 draw order d0..d4).
 static void gen_doorkey(Env& e, DrawStream& ds) {
@@ -333,6 +361,8 @@ void Env::generate() {
     case F_DYNOBS: gen_dynobs(*this, ds); break;
     case F_KEYCORRIDOR: gen_keycorridor(*this, ds); break;
     case F_LAVAGAP: gen_lavagap(*this, ds); break;
+    case F_EMPTY_RANDOM: gen_empty_random(*this, ds); break;
+    case F_DISTSHIFT: gen_distshift(*this); break;
   }
   step_count = 0;
   prev_done = false;

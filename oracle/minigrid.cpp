@@ -183,7 +183,20 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     s.height = s.width = a;
     return true;
   };
-  if (square("Empty-", F_EMPTY)) {
+  if (square("Empty-Random-", F_EMPTY_RANDOM)) {
+    // [MG] EmptyEnv(size, agent_start_pos=None): random start cell and direction
+    if (s.size < 5 || s.size > 16) return false;
+    s.max_steps = 4 * s.size * s.size;
+    s.n_actions = 7;
+  } else if (id == "DistShift1" || id == "DistShift2") {
+    // [MG] DistShiftEnv(width=9, height=7, strip2_row=2 / 5) (R#33)
+    s.family = F_DISTSHIFT;
+    s.width = 9;
+    s.height = 7;
+    s.strip2_row = id == "DistShift1" ? 2 : 5;
+    s.max_steps = 4 * 9 * 7;
+    s.n_actions = 7;
+  } else if (square("Empty-", F_EMPTY)) {
     if (s.size < 3 || s.size > 16) return false;
     s.max_steps = 4 * s.size * s.size;  // [MG] EmptyEnv
     s.n_actions = 7;

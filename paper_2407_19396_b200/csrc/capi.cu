@@ -84,7 +84,12 @@ int parse_id(const char* env_id, EnvConfig* c) {
   int a = 0, b = 0;
   char tail = 0;
   auto sq = [&](const char* fmt) { return sscanf(id.c_str(), fmt, &a, &b, &tail) == 2 && a == b; };
-  if (sq("Empty-%dx%d%c")) {
+  if (sq("Empty-Random-%dx%d%c")) {
+    if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
+    *c = EnvConfig{FAM_EMPTY_RANDOM, a, a, 4 * a * a, 7, 0, 0, 0};
+  } else if (id == "DistShift1" || id == "DistShift2") {  // [MG] DistShiftEnv 9x7 (R#33)
+    *c = EnvConfig{id == "DistShift1" ? FAM_DISTSHIFT1 : FAM_DISTSHIFT2, 7, 9, 4 * 9 * 7, 7, 0, 0, 0};
+  } else if (sq("Empty-%dx%d%c")) {
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     *c = EnvConfig{FAM_EMPTY, a, a, 4 * a * a, 7, 0, 0, 0};
   } else if (sq("DoorKey-%dx%d%c")) {
@@ -113,7 +118,7 @@ void fill_spec(const EnvConfig& c, navix_spec* s) {
   s->n_actions = c.n_actions;
   s->max_steps = c.max_steps;
   s->obs_bytes = OBS_BYTES;
-  s->family = c.family;
+  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family;
   s->n_obstacles = c.n_obstacles;
   s->export_bytes = 3 * c.height * c.width + 12 + 2 * c.n_obstacles;
 }

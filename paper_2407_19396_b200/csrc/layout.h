@@ -51,7 +51,8 @@ constexpr uint8_t CELL_WALL = make_cell(K_WALL, COL_GREY);
 constexpr uint8_t CELL_GOAL = make_cell(K_GOAL, COL_GREEN);
 constexpr uint8_t CELL_LAVA = make_cell(K_LAVA, COL_RED);
 
-enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4 };
+enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4,
+                    FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7 };
 
 struct EnvConfig {
   int family;

@@ -36,7 +36,14 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
     if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
     else wall = x == 0 || y == 0 || x == W - 1 || y == H - 1;
     uint8_t c = wall ? CELL_WALL : CELL_EMPTY;
-    if (FAM != FAM_KEYCORRIDOR && x == W - 2 && y == H - 2) c = CELL_GOAL;  // goal (W-2, H-2)
+    if (FAM == FAM_DISTSHIFT1 || FAM == FAM_DISTSHIFT2) {
+      // [MG] DistShiftEnv: goal (W-2, 1), lava x = 3 .. W-4 on rows 1 and strip2_row (R#33)
+      const int strip2 = FAM == FAM_DISTSHIFT1 ? 2 : 5;
+      if (x == W - 2 && y == 1) c = CELL_GOAL;
+      if (x >= 3 && x < W - 3 && (y == 1 || y == strip2)) c = CELL_LAVA;
+    } else if (FAM != FAM_KEYCORRIDOR && x == W - 2 && y == H - 2) {
+      c = CELL_GOAL;  // goal (W-2, H-2)
+    }
     r |= (uint64_t)c << (8 * (x - x0));
   }
   return r;
@@ -102,7 +109,15 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
   for (int p = 0; p < H * C::RW; ++p) g.rows[p * TILE] = template_plane<FAM, H, W>(p);
   DrawStream ds(genv, episode, 0u, klo, khi);
 
-  if constexpr (FAM == FAM_DOORKEY) {
+  if constexpr (FAM == FAM_EMPTY_RANDOM) {
+    // [MG] EmptyEnv with agent_start_pos=None: place_agent() over the empty
+    // cells (the goal is the last interior cell in row-major order, so the
+    // admissible set is the first (W-2)(H-2)-1 interior cells), then a direction
+    const uint32_t k = ds.next_bounded((uint32_t)((W - 2) * (H - 2) - 1));
+    o.ax = 1 + (int)(k % (W - 2));
+    o.ay = 1 + (int)(k / (W - 2));
+    o.dir = (int)ds.next_bounded(4);
+  } else if constexpr (FAM == FAM_DOORKEY) {
     // [MG] DoorKeyEnv._gen_grid: split, agent pos, agent dir, door row, key pos
     const int split = 2 + (int)ds.next_bounded(W - 4);
     for (int y = 0; y < H; ++y) g.set(split, y, CELL_WALL);

@@ -822,6 +822,12 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
     case FAM_KEYCORRIDOR * 10000 + 1010: return launch_fhw<FAM_KEYCORRIDOR, 10, 10>(mode, a, n_tiles, s);
     case FAM_KEYCORRIDOR * 10000 + 1313: return launch_fhw<FAM_KEYCORRIDOR, 13, 13>(mode, a, n_tiles, s);
     case FAM_KEYCORRIDOR * 10000 + 1616: return launch_fhw<FAM_KEYCORRIDOR, 16, 16>(mode, a, n_tiles, s);
+    case FAM_EMPTY_RANDOM * 10000 + 505: return launch_fhw<FAM_EMPTY_RANDOM, 5, 5>(mode, a, n_tiles, s);
+    case FAM_EMPTY_RANDOM * 10000 + 606: return launch_fhw<FAM_EMPTY_RANDOM, 6, 6>(mode, a, n_tiles, s);
+    case FAM_EMPTY_RANDOM * 10000 + 808: return launch_fhw<FAM_EMPTY_RANDOM, 8, 8>(mode, a, n_tiles, s);
+    case FAM_EMPTY_RANDOM * 10000 + 1616: return launch_fhw<FAM_EMPTY_RANDOM, 16, 16>(mode, a, n_tiles, s);
+    case FAM_DISTSHIFT1 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT1, 7, 9>(mode, a, n_tiles, s);
+    case FAM_DISTSHIFT2 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT2, 7, 9>(mode, a, n_tiles, s);
     default: return cudaErrorInvalidConfiguration;
   }
 }
