@@ -120,6 +120,68 @@ static void gen_distshift(Env& e) {
   e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
 }
 
+// ---------------------------------------------------------------- Crossing
+// [MG] CrossingEnv._gen_grid with obstacle_type = Wall, step by step.  The two
+// np_random.shuffle calls follow R#35: the rivers list is shuffled by a
+// partial Fisher-Yates over its first num_crossings slots (slot k swaps with
+// k + bounded(draw, M - k)), which is all [MG] keeps of it; the path is
+// shuffled by numpy's Fisher-Yates (for i = n-1 .. 1: swap i with
+// bounded(draw, i + 1)).  np_random.choice(range(a, b)) = a + bounded(draw, b - a).
+static void gen_crossing(Env& e, DrawStream& ds) {
+  const int W = e.spec.width, H = e.spec.height, N = e.spec.n_crossings;
+  e.grid = Grid(W, H);
+  e.grid.wall_rect(0, 0, W, H);
+  e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
+  e.grid.set(W - 2, H - 2, make_goal());
+  // rivers = [(v, i) for i in range(2, H-2, 2)] + [(h, j) for j in range(2, W-2, 2)]
+  std::vector<std::pair<char, int>> rivers;
+  for (int i = 2; i < H - 2; i += 2) rivers.push_back({'v', i});
+  for (int j = 2; j < W - 2; j += 2) rivers.push_back({'h', j});
+  const int M = (int)rivers.size();
+  for (int k = 0; k < N; ++k) {
+    int j = k + (int)ds.next_bounded((uint32_t)(M - k));
+    std::swap(rivers[k], rivers[j]);
+  }
+  rivers.resize(N);
+  std::vector<int> rivers_v, rivers_h;
+  for (auto& r : rivers) (r.first == 'v' ? rivers_v : rivers_h).push_back(r.second);
+  std::sort(rivers_v.begin(), rivers_v.end());
+  std::sort(rivers_h.begin(), rivers_h.end());
+  // obstacle_pos = product(range(1, W-1), rivers_h) ++ product(rivers_v, range(1, H-1))
+  for (int i = 1; i < W - 1; ++i)
+    for (int j : rivers_h) e.grid.set(i, j, make_wall());
+  for (int i : rivers_v)
+    for (int j = 1; j < H - 1; ++j) e.grid.set(i, j, make_wall());
+  // path = [h] * len(rivers_v) + [v] * len(rivers_h), shuffled
+  std::vector<char> path;
+  for (size_t k = 0; k < rivers_v.size(); ++k) path.push_back('h');
+  for (size_t k = 0; k < rivers_h.size(); ++k) path.push_back('v');
+  for (int i = (int)path.size() - 1; i >= 1; --i) {
+    int j = (int)ds.next_bounded((uint32_t)(i + 1));
+    std::swap(path[i], path[j]);
+  }
+  // openings
+  std::vector<int> limits_v{0}, limits_h{0};
+  for (int v : rivers_v) limits_v.push_back(v);
+  limits_v.push_back(H - 1);
+  for (int h : rivers_h) limits_h.push_back(h);
+  limits_h.push_back(W - 1);
+  int room_i = 0, room_j = 0;
+  for (char d : path) {
+    int i, j;
+    if (d == 'h') {
+      i = limits_v[room_i + 1];
+      j = limits_h[room_j] + 1 + (int)ds.next_bounded((uint32_t)(limits_h[room_j + 1] - limits_h[room_j] - 1));
+      room_i += 1;
+    } else {
+      i = limits_v[room_i] + 1 + (int)ds.next_bounded((uint32_t)(limits_v[room_i + 1] - limits_v[room_i] - 1));
+      j = limits_h[room_j + 1];
+      room_j += 1;
+    }
+    e.grid.set(i, j, std::nullopt);
+  }
+}
+
 // ---------------------------------------------------------------- DoorKey
 // [MG] DoorKeyEnv._gen_grid (SURVEY §8c-4 draw order d0..d4).
 static void gen_doorkey(Env& e, DrawStream& ds) {
@@ -363,6 +425,7 @@ void Env::generate() {
     case F_LAVAGAP: gen_lavagap(*this, ds); break;
     case F_EMPTY_RANDOM: gen_empty_random(*this, ds); break;
     case F_DISTSHIFT: gen_distshift(*this); break;
+    case F_CROSSING: gen_crossing(*this, ds); break;
   }
   step_count = 0;
   prev_done = false;

@@ -196,11 +196,30 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     s.strip2_row = id == "DistShift1" ? 2 : 5;
     s.max_steps = 4 * 9 * 7;
     s.n_actions = 7;
+  } else if (starts_with(id, "SimpleCrossingS") || starts_with(id, "Crossings-S")) {
+    // [MG] CrossingEnv(size, num_crossings, obstacle_type=Wall); Table 9 also
+    // spells it "Crossings-S9N1" (R#35)
+    pos = starts_with(id, "SimpleCrossingS") ? 15 : 11;
+    int S, N;
+    if (!parse_int(id, pos, &S)) return false;
+    if (pos >= id.size() || id[pos] != 'N') return false;
+    ++pos;
+    if (!parse_int(id, pos, &N) || pos != id.size()) return false;
+    if (S < 5 || S > 16 || S % 2 == 0) return false;  // [MG] asserts odd sizes
+    if (N < 1 || N > 2 * ((S - 3) / 2)) return false;   // at most every river
+    s.family = F_CROSSING;
+    s.size = S;
+    s.height = s.width = S;
+    s.n_crossings = N;
+    s.max_steps = 4 * S * S;  // [MG] CrossingEnv
+    s.n_actions = 7;
   } else if (square("Empty-", F_EMPTY)) {
     if (s.size < 3 || s.size > 16) return false;
     s.max_steps = 4 * s.size * s.size;  // [MG] EmptyEnv
     s.n_actions = 7;
-  } else if (square("DoorKey-", F_DOORKEY)) {
+  } else if (square("DoorKey-", F_DOORKEY) || square("DoorKey-Random-", F_DOORKEY)) {
+    // DoorKey-Random-SxS: [MG]'s DoorKey already draws the agent's cell and
+    // direction, so the Random ids are the same generator (R#36)
     if (s.size < 5 || s.size > 16) return false;
     s.max_steps = 10 * s.size * s.size;  // [MG] DoorKeyEnv
     s.n_actions = 7;

@@ -35,7 +35,7 @@ enum : int { A_LEFT = 0, A_RIGHT = 1, A_FORWARD = 2, A_PICKUP = 3, A_DROP = 4, A
 
 // Families of Table 9 implemented by the oracle.
 enum Family : int { F_EMPTY = 0, F_DOORKEY = 1, F_DYNOBS = 2, F_KEYCORRIDOR = 3, F_LAVAGAP = 4, F_EMPTY_RANDOM = 5,
-                    F_DISTSHIFT = 6 };
+                    F_DISTSHIFT = 6, F_CROSSING = 7 };
 
 // One MiniGrid WorldObj.  `tag` is test-only bookkeeping (rotation pin P6).
 struct Obj {
@@ -93,6 +93,7 @@ struct Spec {
   int num_rows;       // KeyCorridor R
   int n_obstacles;    // DynObs
   int strip2_row;     // DistShift
+  int n_crossings;    // SimpleCrossing N
 };
 // Parses "Navix-DoorKey-8x8-v0" / "MiniGrid-…" / bare ids. false if unknown.
 bool parse_env_id(const std::string& env_id, Spec* out);

@@ -89,10 +89,14 @@ int parse_id(const char* env_id, EnvConfig* c) {
     *c = EnvConfig{FAM_EMPTY_RANDOM, a, a, 4 * a * a, 7, 0, 0, 0};
   } else if (id == "DistShift1" || id == "DistShift2") {  // [MG] DistShiftEnv 9x7 (R#33)
     *c = EnvConfig{id == "DistShift1" ? FAM_DISTSHIFT1 : FAM_DISTSHIFT2, 7, 9, 4 * 9 * 7, 7, 0, 0, 0};
+  } else if (sscanf(id.c_str(), "SimpleCrossingS%dN%d%c", &a, &b, &tail) == 2 ||
+             sscanf(id.c_str(), "Crossings-S%dN%d%c", &a, &b, &tail) == 2) {  // [MG] CrossingEnv (R#35)
+    if (!((a == 9 && b >= 1 && b <= 3) || (a == 11 && b == 5))) return 1;
+    *c = EnvConfig{FAM_CROSSING, a, a, 4 * a * a, 7, 0, 0, 0, b};
   } else if (sq("Empty-%dx%d%c")) {
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     *c = EnvConfig{FAM_EMPTY, a, a, 4 * a * a, 7, 0, 0, 0};
-  } else if (sq("DoorKey-%dx%d%c")) {
+  } else if (sq("DoorKey-%dx%d%c") || sq("DoorKey-Random-%dx%d%c")) {  // R#36
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     *c = EnvConfig{FAM_DOORKEY, a, a, 10 * a * a, 7, 0, 0, 0};
   } else if (sq("Dynamic-Obstacles-%dx%d%c")) {
@@ -118,7 +122,8 @@ void fill_spec(const EnvConfig& c, navix_spec* s) {
   s->n_actions = c.n_actions;
   s->max_steps = c.max_steps;
   s->obs_bytes = OBS_BYTES;
-  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family;
+  // public NAVIX_FAMILY_* ids: DistShift1/2 share one, SimpleCrossing is 7
+  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family == FAM_CROSSING ? 7 : c.family;
   s->n_obstacles = c.n_obstacles;
   s->export_bytes = 3 * c.height * c.width + 12 + 2 * c.n_obstacles;
 }
@@ -139,6 +144,7 @@ KernelArgs make_args(navix_env* h) {
   a.reward_mode = h->reward_mode;
   a.time_cost = h->time_cost;
   a.action_cost = h->action_cost;
+  a.gen_param = h->cfg.gen_param;
   return a;
 }
 

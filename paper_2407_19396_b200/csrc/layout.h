@@ -52,7 +52,7 @@ constexpr uint8_t CELL_GOAL = make_cell(K_GOAL, COL_GREEN);
 constexpr uint8_t CELL_LAVA = make_cell(K_LAVA, COL_RED);
 
 enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4,
-                    FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7 };
+                    FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7, FAM_CROSSING = 8 };
 
 struct EnvConfig {
   int family;
@@ -61,6 +61,7 @@ struct EnvConfig {
   int n_actions;
   int n_obstacles;
   int room_size, num_rows;  // KeyCorridor
+  int gen_param;            // SimpleCrossing: number of crossings N
 };
 
 // Byte offsets of the arrays inside one state allocation.
@@ -121,6 +122,7 @@ struct KernelArgs {
   int bulk_obs;         // 1: obs base is 16-B aligned -> cp.async.bulk store of full tiles
   int bulk_act;         // 1: actions base is 16-B aligned -> cp.async.bulk load of full tiles
   int64_t rollout_steps;  // K of navix_rollout
+  int gen_param;        // EnvConfig::gen_param (runtime level-generator parameter)
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };

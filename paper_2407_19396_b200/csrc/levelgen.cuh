@@ -102,7 +102,7 @@ __device__ __forceinline__ int select_bits(const uint64_t (&m)[NW], uint32_t k) 
 
 template <int FAM, int H, int W>
 __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, uint32_t genv, uint32_t episode,
-                                              uint32_t klo, uint32_t khi) {
+                                              uint32_t klo, uint32_t khi, int gparam) {
   using C = Cfg<FAM, H, W>;
   GenOut o{1, 1, 0, 0u, 0u};
 #pragma unroll
@@ -117,6 +117,56 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     o.ax = 1 + (int)(k % (W - 2));
     o.ay = 1 + (int)(k / (W - 2));
     o.dir = (int)ds.next_bounded(4);
+  } else if constexpr (FAM == FAM_CROSSING) {
+    // [MG] CrossingEnv._gen_grid, obstacle Wall, N = gparam crossings; the two
+    // shuffles as R#35 reads them.  Rivers are nibbles (bit 3: horizontal,
+    // bits 0-2: position / 2 - 1): (S-3)/2 vertical ones, then as many horizontal.
+    constexpr int NRV = (W - 3) / 2, M = 2 * NRV;
+    const int N = gparam;
+    uint64_t riv = 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) riv |= (uint64_t)((k < NRV ? 0 : 8) | (k % NRV)) << (4 * k);
+    uint32_t vmask = 0, hmask = 0;  // bit p: a vertical river at x = p / a horizontal one at y = p
+    for (int k = 0; k < N; ++k) {
+      const int j = k + (int)ds.next_bounded((uint32_t)(M - k));
+      const uint64_t a = (riv >> (4 * k)) & 15, b = (riv >> (4 * j)) & 15;
+      riv = (riv & ~(15ull << (4 * k)) & ~(15ull << (4 * j))) | (b << (4 * k)) | (a << (4 * j));
+      const uint32_t bit = 1u << (2 * ((b & 7) + 1));
+      if (b & 8) hmask |= bit; else vmask |= bit;
+    }
+#pragma unroll
+    for (int y = 1; y < H - 1; ++y)
+#pragma unroll
+      for (int x = 1; x < W - 1; ++x)
+        if (((hmask >> y) & 1u) | ((vmask >> x) & 1u)) g.set(x, y, CELL_WALL);
+    // path: popc(vmask) 'h' moves then popc(hmask) 'v' moves (bit k = 1: 'v'), Fisher-Yates
+    const int nv = __popc(vmask);
+    uint32_t path = ((1u << N) - 1) & ~((1u << nv) - 1);
+    for (int i = N - 1; i >= 1; --i) {
+      const int j = (int)ds.next_bounded((uint32_t)(i + 1));
+      const uint32_t bi = (path >> i) & 1u, bj = (path >> j) & 1u;
+      path = (path & ~(1u << i) & ~(1u << j)) | (bj << i) | (bi << j);
+    }
+    // openings: the current room spans x in (xlo, xhi), y in (ylo, yhi)
+    auto next_limit = [](uint32_t m, int lo, int end) {
+      const uint32_t above = m & ~((2u << lo) - 1);
+      return above ? __ffs(above) - 1 : end;
+    };
+    int xlo = 0, ylo = 0;
+    int xhi = next_limit(vmask, 0, W - 1), yhi = next_limit(hmask, 0, H - 1);
+    for (int k = 0; k < N; ++k) {
+      if (((path >> k) & 1u) == 0) {  // 'h': through the vertical river at x = xhi
+        const int y = ylo + 1 + (int)ds.next_bounded((uint32_t)(yhi - ylo - 1));
+        g.set(xhi, y, CELL_EMPTY);
+        xlo = xhi;
+        xhi = next_limit(vmask, xlo, W - 1);
+      } else {                        // 'v': through the horizontal river at y = yhi
+        const int x = xlo + 1 + (int)ds.next_bounded((uint32_t)(xhi - xlo - 1));
+        g.set(x, yhi, CELL_EMPTY);
+        ylo = yhi;
+        yhi = next_limit(hmask, ylo, H - 1);
+      }
+    }
   } else if constexpr (FAM == FAM_DOORKEY) {
     // [MG] DoorKeyEnv._gen_grid: split, agent pos, agent dir, door row, key pos
     const int split = 2 + (int)ds.next_bounded(W - 4);

@@ -245,7 +245,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       const int st = s_q[q];
       const uint32_t genv_t = a.env_begin + (uint32_t)(tile0 + env_of_slot(st));
       const GenOut o =
-          generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi);
+          generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi,
+                                    a.gen_param);
       s_qballs[st] = o.balls;
       s_qout[st] = (uint32_t)o.ax | ((uint32_t)o.ay << 8) | ((uint32_t)o.dir << 16) | (o.fail << 24);
     }
@@ -267,7 +268,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       if (!in.episode_known) episode = a.episode[slot];
       episode += 1;
     }
-    const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi);
+    const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi, a.gen_param);
     ax = o.ax; ay = o.ay; dir = o.dir;
     balls = o.balls;
     st_fail = o.fail;
@@ -828,6 +829,8 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
     case FAM_EMPTY_RANDOM * 10000 + 1616: return launch_fhw<FAM_EMPTY_RANDOM, 16, 16>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT1 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT1, 7, 9>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT2 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT2, 7, 9>(mode, a, n_tiles, s);
+    case FAM_CROSSING * 10000 + 909: return launch_fhw<FAM_CROSSING, 9, 9>(mode, a, n_tiles, s);
+    case FAM_CROSSING * 10000 + 1111: return launch_fhw<FAM_CROSSING, 11, 11>(mode, a, n_tiles, s);
     default: return cudaErrorInvalidConfiguration;
   }
 }

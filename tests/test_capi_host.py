@@ -28,6 +28,12 @@ def test_header_symbols_are_exported():
     ("Navix-KeyCorridorS3R3-v0", 7, 7, 270, 7, 3),
     ("KeyCorridorS3R1", 3, 7, 270, 7, 3),
     ("Navix-LavaGapS7-v0", 7, 7, 196, 7, 4),
+    ("Navix-Empty-Random-6x6", 6, 6, 144, 7, 5),
+    ("Navix-DistShift1-v0", 7, 9, 252, 7, 6),
+    ("Navix-DistShift2-v0", 7, 9, 252, 7, 6),
+    ("Navix-SimpleCrossingS9N2-v0", 9, 9, 324, 7, 7),
+    ("Navix-Crossings-S11N5-v0", 11, 11, 484, 7, 7),
+    ("Navix-DoorKey-Random-5x5", 5, 5, 250, 7, 1),
 ])
 def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     from oracle import spec_of as oracle_spec
@@ -36,6 +42,7 @@ def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     assert (s.height, s.width, s.max_steps, s.n_actions, s.family, s.obs_bytes, s.view) == (h, w, T, na, fam, 147, 7)
     o = oracle_spec(env_id)  # the two independent parsers agree
     assert (o.height, o.width, o.max_steps, o.n_actions, o.export_bytes) == (h, w, T, na, s.export_bytes)
+    assert o.family == fam
 
 
 def test_unknown_ids_and_row_f2_sizes():

@@ -114,3 +114,73 @@ def test_empty_random_goal_reward_from_known_start():
     env.step(np.array([R], np.uint8))                   # south
     _, r, te, _ = env.step(np.array([F], np.uint8))     # goal (4,4)
     assert te[0] == 1 and float(r[0]) == pytest.approx(1 - 0.9 * 4 / 144, abs=1e-7)
+
+
+def _crossing_levels(env_id, n, seed=7):
+    env = OracleEnv(env_id, n, seed=seed)
+    env.reset()
+    return env.observe_full()[:, :, :, 0]  # [n][x][y] type
+
+
+def _reachable(t, sx, sy):
+    S = t.shape[0]
+    seen = np.zeros_like(t, bool)
+    st = [(sx, sy)]
+    seen[sx, sy] = True
+    while st:
+        x, y = st.pop()
+        for dx, dy in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+            u, v = x + dx, y + dy
+            if 0 <= u < S and 0 <= v < S and not seen[u, v] and t[u, v] != 2:
+                seen[u, v] = True
+                st.append((u, v))
+    return seen
+
+
+@pytest.mark.parametrize("env_id,S,N", [("SimpleCrossingS9N1-v0", 9, 1), ("SimpleCrossingS9N2-v0", 9, 2),
+                                        ("SimpleCrossingS9N3-v0", 9, 3), ("Crossings-S11N5-v0", 11, 5)])
+def test_crossing_structure_and_solvable(env_id, S, N):
+    s = spec_of(env_id)
+    assert (s.width, s.height, s.max_steps, s.n_actions) == (S, S, 4 * S * S, 7)
+    levels = _crossing_levels(env_id, 400)
+    for t in levels:
+        assert t[1, 1] == 10 and t[S - 2, S - 2] == 8
+        # a river line holds S-3 walls (its one opening excepted); any other
+        # interior line holds at most N walls (where rivers cross it) < S-3
+        cols = [x for x in range(1, S - 1) if np.count_nonzero(t[x, 1:-1] == 2) == S - 3]
+        rows = [y for y in range(1, S - 1) if np.count_nonzero(t[1:-1, y] == 2) == S - 3]
+        assert all(x % 2 == 0 and 2 <= x <= S - 3 for x in cols)
+        assert all(y % 2 == 0 and 2 <= y <= S - 3 for y in rows)
+        assert len(cols) + len(rows) == N
+        want = np.zeros((S, S), bool)
+        for x in cols:
+            want[x, 1:-1] = True
+        for y in rows:
+            want[1:-1, y] = True
+        interior = np.pad(np.ones((S - 2, S - 2), bool), 1)
+        got = t == 2
+        assert not np.any(got & interior & ~want)      # no wall off the rivers
+        assert np.count_nonzero(want & ~got) == N      # exactly one opening per river
+        assert _reachable(t, 1, 1)[S - 2, S - 2]       # the openings connect start and goal
+
+
+def test_crossing_river_subset_and_opening_uniform():
+    # S9N2: the 2 rivers are a uniform 2-subset of the 6 candidates (C(6,2) = 15)
+    lv = _crossing_levels("SimpleCrossingS9N2-v0", 6000, seed=9)
+    keys = []
+    for t in lv:
+        v = tuple(x for x in (2, 4, 6) if np.count_nonzero(t[x, 1:-1] == 2) >= 5)
+        h = tuple(y for y in (2, 4, 6) if np.count_nonzero(t[1:-1, y] == 2) >= 5)
+        keys.append((v, h))
+    _, cnt = np.unique(np.array([str(k) for k in keys]), return_counts=True)
+    assert len(cnt) == 15 and sps.chisquare(cnt).pvalue > 1e-4
+    # S9N1 with a vertical river: its opening row is uniform over 1..7
+    lv = _crossing_levels("SimpleCrossingS9N1-v0", 8000, seed=10)
+    ys = []
+    for t in lv:
+        for x in (2, 4, 6):
+            col = t[x, 1:-1]
+            if np.count_nonzero(col == 2) == 6:
+                ys.append(1 + int(np.argmax(col != 2)))
+    c = np.bincount(ys, minlength=8)[1:]
+    assert len(ys) > 3000 and sps.chisquare(c).pvalue > 1e-4
