@@ -355,7 +355,7 @@ def run_navix(args, rank, world, local_rank):
         "rollout": rollout,
         "clocks": clk.summary(),
         "episode_stats": {k: int(v) for k, v in zip(
-            ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_collision", "n_truncated",
+            ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_failure", "n_truncated",
              "gen_failures"), st)},
         "mean_episode_return_minigrid": mean_legacy_return(st, spec.max_steps),
         "host": {"cpu_model": model, "nproc": ncpu},

@@ -63,7 +63,8 @@ enum {
   NAVIX_FAMILY_LAVAGAP = 4,
   NAVIX_FAMILY_EMPTY_RANDOM = 5,
   NAVIX_FAMILY_DISTSHIFT = 6,
-  NAVIX_FAMILY_CROSSING = 7
+  NAVIX_FAMILY_CROSSING = 7,
+  NAVIX_FAMILY_GOTODOOR = 8
 };
 
 /* Reward modes (R#1/R#3): MINIGRID = legacy 1 - 0.9*sc/T on success,
@@ -120,7 +121,8 @@ NAVIX_API navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream);
  *  actions     (dev) uint8[n]
  *  obs         (dev) uint8[n][7][7][3] (16-byte aligned: bulk-store fast path)
  *  reward      (dev) float[n]     (R#1/R#2/R#3, R_3 = -1 on collision R#4)
- *  terminated  (dev) uint8[n]     0/1 (event: goal, lava, collision, KeyCorridor ball)
+ *  terminated  (dev) uint8[n]     0/1 (event: goal, lava, collision, KeyCorridor ball,
+ *                                  GoToDoor toggle / done, R#37)
  *  truncated   (dev) uint8[n]     0/1 (step_count reached T without an event, R#17)
  * An env whose previous step ended ignores its action, starts its next
  * episode and returns that episode's first observation with reward 0 and
@@ -169,7 +171,8 @@ NAVIX_API navix_status navix_step_host(navix_env* h, const uint8_t* actions, uin
 
 /* Episode statistics of this shard since the last reset (info i_{t+1},
  * P:238): out8 (dev) int64[8] = {episodes, sum of lengths, n_success,
- * sum of step counts at success, n_lava, n_collision, n_truncated,
+ * sum of step counts at success, n_lava, n_failure (Dynamic-Obstacles
+ * collision; GoToDoor toggle or done away from the target), n_truncated,
  * generator failures}.  Exact integers: summing over shards (an all-reduce)
  * gives the unsharded values. */
 NAVIX_API navix_status navix_stats(navix_env* h, int64_t* out8, void* stream);
@@ -178,10 +181,12 @@ NAVIX_API navix_status navix_stats(navix_env* h, int64_t* out8, void* stream);
  *   H*W cells as MiniGrid (type, colour, state), row-major y outer, x inner;
  *   agent x, y, dir; carry (type, colour), (1, 0) = nothing;
  *   step_count u16; episode u32; prev_done u8;
- *   Dynamic-Obstacles: n_obstacles x (x, y) in creation order.
+ *   Dynamic-Obstacles: n_obstacles x (x, y) in creation order;
+ *   GoToDoor: the target door's (x, y).
  * export: synchronises the device, writes n*export_bytes into `host`.
  * import: validates every record (closed wall border, agent on a walkable
- * interior cell, legal codes, balls consistent) before touching the device. */
+ * interior cell, legal codes, balls consistent; GoToDoor: any border, agent
+ * anywhere walkable, target inside the grid) before touching the device. */
 NAVIX_API navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* written);
 NAVIX_API navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes);
 

@@ -42,8 +42,10 @@ def random_actions(seed: int, steps: int, n: int, n_actions: int, high: int | No
 
 def record_from_map(rows: list[str], agent_dir: int, *, carry=(EMPTY, 0), step_count: int = 0,
                     episode: int = 0, prev_done: int = 0, colors: dict | None = None,
-                    balls: list[tuple[int, int]] | None = None) -> np.ndarray:
-    """Canonical record for one env from an ASCII map (rows = y, columns = x)."""
+                    balls: list[tuple[int, int]] | None = None,
+                    target: tuple[int, int] | None = None) -> np.ndarray:
+    """Canonical record for one env from an ASCII map (rows = y, columns = x);
+    `target` = GoToDoor's target door (x, y), appended last."""
     H, W = len(rows), len(rows[0])
     colors = colors or {}
     out = []
@@ -64,6 +66,8 @@ def record_from_map(rows: list[str], agent_dir: int, *, carry=(EMPTY, 0), step_c
     out += [prev_done]
     for bx, by in balls or []:
         out += [bx, by]
+    if target is not None:
+        out += list(target)
     return np.array(out, np.uint8)
 
 
@@ -86,24 +90,27 @@ def decode_record(rec: np.ndarray, H: int, W: int, n_obstacles: int = 0) -> dict
 
 
 def random_records(seed: int, n: int, H: int, W: int, max_steps: int, n_obstacles: int = 0,
-                   p_prev_done: float = 0.0) -> np.ndarray:
+                   p_prev_done: float = 0.0, open_edge: bool = False) -> np.ndarray:
     """n canonical records of random but legal states: wall border, random
     interior objects (walls, doors in all three states, keys, balls, boxes,
     goals, lava, floor), the agent on a walkable interior cell, a random
     carried object, random step count.  With n_obstacles > 0 (DynObs) exactly
     that many blue balls are listed (extra balls may still appear as static
-    objects)."""
+    objects).  open_edge (GoToDoor records): the border cells are random too,
+    the agent may stand on any walkable cell, and a random target door
+    position (x, y) inside the grid ends the record."""
     rng = np.random.default_rng(seed)
     kinds = np.array([EMPTY, WALL, DOOR, KEY, BALL, BOX, GOAL, LAVA, FLOOR])
     probs = np.array([0.42, 0.16, 0.12, 0.07, 0.06, 0.04, 0.05, 0.05, 0.03])
-    per = 3 * H * W + 12 + 2 * n_obstacles
+    per = 3 * H * W + 12 + 2 * n_obstacles + (2 if open_edge else 0)
     out = np.zeros((n, per), np.uint8)
+    m = 0 if open_edge else 1
     for e in range(n):
         cells = np.zeros((H, W, 3), np.uint8)
         cells[:, :, 0] = WALL
         cells[:, :, 1] = GREY
-        for y in range(1, H - 1):
-            for x in range(1, W - 1):
+        for y in range(m, H - m):
+            for x in range(m, W - m):
                 k = rng.choice(kinds, p=probs)
                 c = int(rng.integers(0, 6))
                 if k == EMPTY:
@@ -112,7 +119,7 @@ def random_records(seed: int, n: int, H: int, W: int, max_steps: int, n_obstacle
                     cells[y, x] = (DOOR, c, int(rng.integers(0, 3)))
                 else:
                     cells[y, x] = (k, c, 0)
-        walk = [(x, y) for y in range(1, H - 1) for x in range(1, W - 1)
+        walk = [(x, y) for y in range(m, H - m) for x in range(m, W - m)
                 if cells[y, x, 0] in (EMPTY, FLOOR, GOAL, LAVA) or (cells[y, x, 0] == DOOR and cells[y, x, 2] == OPEN)]
         if not walk:
             x, y = 1, 1
@@ -137,5 +144,7 @@ def random_records(seed: int, n: int, H: int, W: int, max_steps: int, n_obstacle
         rec += [int(rng.random() < p_prev_done)]
         for bx, by in balls:
             rec += [bx, by]
+        if open_edge:
+            rec += [int(rng.integers(0, W)), int(rng.integers(0, H))]
         out[e] = rec
     return out

@@ -15,7 +15,7 @@ _lib = None
 
 STATS_FIELDS = (
     "episodes", "sum_len", "n_success", "sum_success_step",
-    "n_lava", "n_collision", "n_truncated", "gen_failures",
+    "n_lava", "n_failure", "n_truncated", "gen_failures",
 )
 
 

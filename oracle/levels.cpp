@@ -182,6 +182,38 @@ static void gen_crossing(Env& e, DrawStream& ds) {
   }
 }
 
+// ---------------------------------------------------------------- GoToDoor
+// [MG] GoToDoorEnv._gen_grid, step by step.  _rand_int(a, b) = a +
+// bounded(draw, b - a); the colour loop (rand_elem until unused) is one draw
+// over the unused colours in COLOR_NAMES order (R#37, as R#20).
+static void gen_gotodoor(Env& e, DrawStream& ds) {
+  const int S = e.spec.size;
+  e.grid = Grid(S, S);
+  const int w = 5 + (int)ds.next_bounded((uint32_t)(S + 1 - 5));
+  const int h = 5 + (int)ds.next_bounded((uint32_t)(S + 1 - 5));
+  e.grid.wall_rect(0, 0, w, h);
+  int dx[4], dy[4];
+  dx[0] = 2 + (int)ds.next_bounded((uint32_t)(w - 4)); dy[0] = 0;
+  dx[1] = 2 + (int)ds.next_bounded((uint32_t)(w - 4)); dy[1] = h - 1;
+  dx[2] = 0; dy[2] = 2 + (int)ds.next_bounded((uint32_t)(h - 4));
+  dx[3] = w - 1; dy[3] = 2 + (int)ds.next_bounded((uint32_t)(h - 4));
+  std::vector<int> unused{0, 1, 2, 3, 4, 5}, colors;
+  while (colors.size() < 4) {
+    int k = (int)ds.next_bounded((uint32_t)unused.size());
+    colors.push_back(unused[k]);
+    unused.erase(unused.begin() + k);
+  }
+  for (int i = 0; i < 4; ++i) e.grid.set(dx[i], dy[i], make_door((uint8_t)colors[i], false));
+  // place_agent(size=(w, h)): position then direction
+  e.agent_x = -1; e.agent_y = -1;
+  int ax, ay;
+  place_uniform(e, 0, 0, w, h, ds.next(), nullptr, &ax, &ay);
+  e.agent_x = ax; e.agent_y = ay;
+  e.agent_dir = (int)ds.next_bounded(4);
+  const int t = (int)ds.next_bounded(4);
+  e.target_x = dx[t]; e.target_y = dy[t];
+}
+
 // ---------------------------------------------------------------- DoorKey
 // [MG] DoorKeyEnv._gen_grid (SURVEY §8c-4 draw order d0..d4).
 static void gen_doorkey(Env& e, DrawStream& ds) {
@@ -426,6 +458,7 @@ void Env::generate() {
     case F_EMPTY_RANDOM: gen_empty_random(*this, ds); break;
     case F_DISTSHIFT: gen_distshift(*this); break;
     case F_CROSSING: gen_crossing(*this, ds); break;
+    case F_GOTODOOR: gen_gotodoor(*this, ds); break;
   }
   step_count = 0;
   prev_done = false;

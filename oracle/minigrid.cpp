@@ -12,6 +12,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include <cstdlib>
+
 #include "oracle.hpp"
 
 namespace oracle {
@@ -213,6 +215,11 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     s.n_crossings = N;
     s.max_steps = 4 * S * S;  // [MG] CrossingEnv
     s.n_actions = 7;
+  } else if (square("GoToDoor-", F_GOTODOOR)) {
+    // [MG] GoToDoorEnv(size): a random room of 5..size cells per side, 4 doors
+    if (s.size < 5 || s.size > 16) return false;
+    s.max_steps = 4 * s.size * s.size;
+    s.n_actions = 7;
   } else if (square("Empty-", F_EMPTY)) {
     if (s.size < 3 || s.size > 16) return false;
     s.max_steps = 4 * s.size * s.size;  // [MG] EmptyEnv
@@ -334,7 +341,10 @@ StepOut Env::step(int action) {
   bool terminated = false;
   bool success = false, lava = false, collision = false;
   auto fp = front_pos();
-  Cell fwd_cell = grid.get(fp.first, fp.second);  // re-read after the balls moved
+  // re-read after the balls moved; outside the grid reads as a Wall, as
+  // gen_obs_grid's slice does (R#37: only GoToDoor's open grid edge gets there)
+  const bool fp_in = fp.first >= 0 && fp.second >= 0 && fp.first < grid.width && fp.second < grid.height;
+  Cell fwd_cell = fp_in ? grid.get(fp.first, fp.second) : Cell(make_wall());
   switch (action) {
     case A_LEFT:
       agent_dir -= 1;
@@ -394,6 +404,22 @@ StepOut Env::step(int action) {
       // done (6) is a no-op; actions >= 7 are no-ops too (R#15)
       break;
   }
+  bool failure = false;
+  if (S.family == F_GOTODOOR) {
+    // [MG] GoToDoorEnv.step: toggle ends the episode (the door is already
+    // toggled); done ends it, with the success reward iff the agent is next
+    // to the target door (R#37)
+    if (action == A_TOGGLE) terminated = true;
+    if (action == A_DONE) {
+      if ((agent_x == target_x && std::abs(agent_y - target_y) == 1) ||
+          (agent_y == target_y && std::abs(agent_x - target_x) == 1)) {
+        reward = success_reward(reward_mode, step_count, S.max_steps);
+        success = true;
+      }
+      terminated = true;
+    }
+    failure = (action == A_TOGGLE || action == A_DONE) && !success;  // not lava / goal (imported states)
+  }
   if (S.family == F_KEYCORRIDOR && action == A_PICKUP && carrying && carrying->type == T_BALL) {
     // [MG] KeyCorridorEnv.step: picking up the target ball (R#8)
     reward = success_reward(reward_mode, step_count, S.max_steps);
@@ -426,7 +452,7 @@ StepOut Env::step(int action) {
     stats[ST_SUM_LEN] += step_count;
     if (success) { stats[ST_SUCCESS] += 1; stats[ST_SUM_SUCCESS_STEP] += step_count; }
     if (lava) stats[ST_LAVA] += 1;
-    if (collision) stats[ST_COLLISION] += 1;
+    if (collision || failure) stats[ST_FAILURE] += 1;
     if (truncated) stats[ST_TRUNCATED] += 1;
   }
   return out;
@@ -466,7 +492,8 @@ void Env::gen_full_obs(uint8_t* out) const {
 
 // ---------------------------------------------------------------- export
 int export_bytes_per_env(const Spec& s) {
-  return 3 * s.height * s.width + 12 + (s.family == F_DYNOBS ? 2 * s.n_obstacles : 0);
+  return 3 * s.height * s.width + 12 + (s.family == F_DYNOBS ? 2 * s.n_obstacles : 0) +
+         (s.family == F_GOTODOOR ? 2 : 0);
 }
 
 static void put16(uint8_t* p, uint32_t v) { p[0] = v & 0xff; p[1] = (v >> 8) & 0xff; }
@@ -499,6 +526,7 @@ void export_env(const Env& e, uint8_t* out) {
     for (int b = 0; b < s.n_obstacles; ++b) {
       p[0] = (uint8_t)e.obstacles[b].first; p[1] = (uint8_t)e.obstacles[b].second; p += 2;
     }
+  if (s.family == F_GOTODOOR) { p[0] = (uint8_t)e.target_x; p[1] = (uint8_t)e.target_y; }
 }
 
 static bool decode_obj(const uint8_t* t, Cell* out) {
@@ -534,8 +562,10 @@ bool import_env(Env& e, const uint8_t* in) {
       g.set(x, y, c);
       p += 3;
     }
-  // closed border of walls (the invariant R#12 relies on)
-  for (int y = 0; y < s.height; ++y)
+  // closed border of walls (the invariant R#12 relies on); GoToDoor reads
+  // outside the grid as walls everywhere (R#37), so its border is free
+  const bool open_edge = s.family == F_GOTODOOR;
+  for (int y = 0; y < s.height && !open_edge; ++y)
     for (int x = 0; x < s.width; ++x)
       if (x == 0 || y == 0 || x == s.width - 1 || y == s.height - 1) {
         const Cell& c = g.get(x, y);
@@ -543,7 +573,8 @@ bool import_env(Env& e, const uint8_t* in) {
       }
   int ax = p[0], ay = p[1], ad = p[2];
   p += 3;
-  if (ax < 1 || ay < 1 || ax > s.width - 2 || ay > s.height - 2 || ad > 3) return false;
+  const int m = open_edge ? 0 : 1;
+  if (ax < m || ay < m || ax > s.width - 1 - m || ay > s.height - 1 - m || ad > 3) return false;
   const Cell& under = g.get(ax, ay);
   if (under && !under->can_overlap()) return false;
   Cell carry;
@@ -567,7 +598,13 @@ bool import_env(Env& e, const uint8_t* in) {
       obst.push_back({bx, by});
     }
   }
+  int tx = 0, ty = 0;
+  if (s.family == F_GOTODOOR) {
+    tx = p[0]; ty = p[1];
+    if (tx >= s.width || ty >= s.height) return false;
+  }
   e.grid = g;
+  e.target_x = tx; e.target_y = ty;
   e.agent_x = ax; e.agent_y = ay; e.agent_dir = ad;
   e.carrying = carry;
   e.step_count = sc;

@@ -35,7 +35,7 @@ enum : int { A_LEFT = 0, A_RIGHT = 1, A_FORWARD = 2, A_PICKUP = 3, A_DROP = 4, A
 
 // Families of Table 9 implemented by the oracle.
 enum Family : int { F_EMPTY = 0, F_DOORKEY = 1, F_DYNOBS = 2, F_KEYCORRIDOR = 3, F_LAVAGAP = 4, F_EMPTY_RANDOM = 5,
-                    F_DISTSHIFT = 6, F_CROSSING = 7 };
+                    F_DISTSHIFT = 6, F_CROSSING = 7, F_GOTODOOR = 8 };
 
 // One MiniGrid WorldObj.  `tag` is test-only bookkeeping (rotation pin P6).
 struct Obj {
@@ -130,6 +130,7 @@ struct Env {
   uint32_t global_index = 0;  // c0 of every Philox counter (shard invariance)
   Grid grid{1, 1};
   int agent_x = 0, agent_y = 0, agent_dir = 0;
+  int target_x = 0, target_y = 0;  // GoToDoor: [MG] target_pos
   Cell carrying;
   int step_count = 0;
   uint32_t episode = 0;
@@ -146,7 +147,7 @@ struct Env {
 };
 
 // Stats slots.
-enum { ST_EPISODES = 0, ST_SUM_LEN, ST_SUCCESS, ST_SUM_SUCCESS_STEP, ST_LAVA, ST_COLLISION, ST_TRUNCATED, ST_GEN_FAIL };
+enum { ST_EPISODES = 0, ST_SUM_LEN, ST_SUCCESS, ST_SUM_SUCCESS_STEP, ST_LAVA, ST_FAILURE, ST_TRUNCATED, ST_GEN_FAIL };
 
 // Canonical export record size per env.
 int export_bytes_per_env(const Spec& s);

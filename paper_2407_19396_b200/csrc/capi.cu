@@ -93,6 +93,9 @@ int parse_id(const char* env_id, EnvConfig* c) {
              sscanf(id.c_str(), "Crossings-S%dN%d%c", &a, &b, &tail) == 2) {  // [MG] CrossingEnv (R#35)
     if (!((a == 9 && b >= 1 && b <= 3) || (a == 11 && b == 5))) return 1;
     *c = EnvConfig{FAM_CROSSING, a, a, 4 * a * a, 7, 0, 0, 0, b};
+  } else if (sq("GoToDoor-%dx%d%c")) {  // [MG] GoToDoorEnv (R#37)
+    if (a != 5 && a != 6 && a != 8) return 1;
+    *c = EnvConfig{FAM_GOTODOOR, a, a, 4 * a * a, 7, 0, 0, 0};
   } else if (sq("Empty-%dx%d%c")) {
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     *c = EnvConfig{FAM_EMPTY, a, a, 4 * a * a, 7, 0, 0, 0};
@@ -123,9 +126,9 @@ void fill_spec(const EnvConfig& c, navix_spec* s) {
   s->max_steps = c.max_steps;
   s->obs_bytes = OBS_BYTES;
   // public NAVIX_FAMILY_* ids: DistShift1/2 share one, SimpleCrossing is 7
-  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family == FAM_CROSSING ? 7 : c.family;
+  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family == FAM_CROSSING ? 7 : c.family == FAM_GOTODOOR ? 8 : c.family;
   s->n_obstacles = c.n_obstacles;
-  s->export_bytes = 3 * c.height * c.width + 12 + 2 * c.n_obstacles;
+  s->export_bytes = 3 * c.height * c.width + 12 + 2 * c.n_obstacles + (c.family == FAM_GOTODOOR ? 2 : 0);
 }
 
 KernelArgs make_args(navix_env* h) {
@@ -450,6 +453,10 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
       p[0] = (uint8_t)(q >> 4);
       p[1] = (uint8_t)(q & 15);
     }
+    if (c.family == FAM_GOTODOOR) {  // target door: agent record byte 7 = (x << 4) | y
+      p[0] = (uint8_t)(r >> 60);
+      p[1] = (uint8_t)((r >> 56) & 15);
+    }
   }
   return NAVIX_OK;
 }
@@ -474,11 +481,12 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
           return fail(NAVIX_E_INVALID_ARG, "env %lld: illegal cell code (%d,%d,%d) at (%d,%d)", (long long)i, p[0],
                       p[1], p[2], x, y);
         const bool border = x == 0 || y == 0 || x == W - 1 || y == H - 1;
-        if (border && (cells[y][x] & 15) != K_WALL)
+        if (border && c.family != FAM_GOTODOOR && (cells[y][x] & 15) != K_WALL)
           return fail(NAVIX_E_INVALID_ARG, "env %lld: border cell (%d,%d) is not a wall (R#12)", (long long)i, x, y);
       }
     const int ax = p[0], ay = p[1], dir = p[2];
-    if (ax < 1 || ay < 1 || ax > W - 2 || ay > H - 2 || dir > 3)
+    const int m = c.family == FAM_GOTODOOR ? 0 : 1;  // GoToDoor: open grid edge (R#37)
+    if (ax < m || ay < m || ax > W - 1 - m || ay > H - 1 - m || dir > 3)
       return fail(NAVIX_E_INVALID_ARG, "env %lld: agent (%d,%d,%d) not an interior pose", (long long)i, ax, ay, dir);
     if (!walkable_kind(cells[ay][ax] & 15))
       return fail(NAVIX_E_INVALID_ARG, "env %lld: agent stands on a non-walkable cell", (long long)i);
@@ -504,6 +512,12 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
           return fail(NAVIX_E_INVALID_ARG, "env %lld: duplicate obstacle", (long long)i);
       bl |= (uint64_t)((bx << 4) | by) << (8 * b);
     }
+    uint64_t target = 0;
+    if (c.family == FAM_GOTODOOR) {
+      if (p[0] >= W || p[1] >= H)
+        return fail(NAVIX_E_INVALID_ARG, "env %lld: target (%d,%d) outside the grid", (long long)i, p[0], p[1]);
+      target = (uint64_t)((p[0] << 4) | p[1]) << 56;
+    }
     for (int b = 0; b < c.n_obstacles; ++b) {  // balls live outside the HBM grid
       const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
       cells[q & 15][q >> 4] = CELL_EMPTY;
@@ -513,7 +527,7 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
       for (int x = 0; x < W; ++x)
         grid[(size_t)(tile * H * RW + y * RW + x / 8) * TILE + lane] |= (uint64_t)cells[y][x] << (8 * (x % 8));
     agent[si] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-               ((uint64_t)sc << 32) | ((uint64_t)pd << 48);
+               ((uint64_t)sc << 32) | ((uint64_t)pd << 48) | target;
     episode[si] = ep;
     balls[si] = bl;
   }

@@ -24,7 +24,7 @@
 //
 // Agent record (u64, little endian bytes): 0 x, 1 y, 2 dir, 3 carry (cell
 // byte of the carried object, 0x01 = nothing), 4-5 step_count, 6 flags
-// (bit 0 prev_done), 7 unused.
+// (bit 0 prev_done), 7 GoToDoor target door (x << 4) | y (else unused).
 #pragma once
 #include <cstdint>
 
@@ -52,7 +52,8 @@ constexpr uint8_t CELL_GOAL = make_cell(K_GOAL, COL_GREEN);
 constexpr uint8_t CELL_LAVA = make_cell(K_LAVA, COL_RED);
 
 enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4,
-                    FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7, FAM_CROSSING = 8 };
+                    FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7, FAM_CROSSING = 8,
+                    FAM_GOTODOOR = 9 };
 
 struct EnvConfig {
   int family;

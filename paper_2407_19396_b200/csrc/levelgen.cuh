@@ -33,7 +33,8 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
   uint64_t r = 0;
   for (int x = x0; x < x0 + 8 && x < W; ++x) {
     bool wall;
-    if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
+    if (FAM == FAM_GOTODOOR) wall = false;  // the generator draws the room
+    else if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
     else wall = x == 0 || y == 0 || x == W - 1 || y == H - 1;
     uint8_t c = wall ? CELL_WALL : CELL_EMPTY;
     if (FAM == FAM_DISTSHIFT1 || FAM == FAM_DISTSHIFT2) {
@@ -41,7 +42,7 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
       const int strip2 = FAM == FAM_DISTSHIFT1 ? 2 : 5;
       if (x == W - 2 && y == 1) c = CELL_GOAL;
       if (x >= 3 && x < W - 3 && (y == 1 || y == strip2)) c = CELL_LAVA;
-    } else if (FAM != FAM_KEYCORRIDOR && x == W - 2 && y == H - 2) {
+    } else if (FAM != FAM_KEYCORRIDOR && FAM != FAM_GOTODOOR && x == W - 2 && y == H - 2) {
       c = CELL_GOAL;  // goal (W-2, H-2)
     }
     r |= (uint64_t)c << (8 * (x - x0));
@@ -84,6 +85,7 @@ struct GenOut {
   int ax, ay, dir;
   uint64_t balls;  // DynObs: byte b = (x << 4) | y of ball b (up to 8)
   uint32_t fail;
+  uint32_t target;  // GoToDoor: target door (x << 4) | y
 };
 
 // k-th set bit of a multi-word mask (word w covers bits 64w ..).
@@ -104,7 +106,7 @@ template <int FAM, int H, int W>
 __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, uint32_t genv, uint32_t episode,
                                               uint32_t klo, uint32_t khi, int gparam) {
   using C = Cfg<FAM, H, W>;
-  GenOut o{1, 1, 0, 0u, 0u};
+  GenOut o{1, 1, 0, 0u, 0u, 0u};
 #pragma unroll
   for (int p = 0; p < H * C::RW; ++p) g.rows[p * TILE] = template_plane<FAM, H, W>(p);
   DrawStream ds(genv, episode, 0u, klo, khi);
@@ -117,6 +119,38 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     o.ax = 1 + (int)(k % (W - 2));
     o.ay = 1 + (int)(k / (W - 2));
     o.dir = (int)ds.next_bounded(4);
+  } else if constexpr (FAM == FAM_GOTODOOR) {
+    // [MG] GoToDoorEnv._gen_grid: room size, walls, 4 door positions, 4
+    // distinct colours (one draw over the unused ones, R#37), agent, target
+    const int w = 5 + (int)ds.next_bounded((uint32_t)(W - 4));
+    const int h = 5 + (int)ds.next_bounded((uint32_t)(H - 4));
+    for (int x = 0; x < w; ++x) { g.set(x, 0, CELL_WALL); g.set(x, h - 1, CELL_WALL); }
+    for (int y = 1; y < h - 1; ++y) { g.set(0, y, CELL_WALL); g.set(w - 1, y, CELL_WALL); }
+    const int d0 = 2 + (int)ds.next_bounded((uint32_t)(w - 4));
+    const int d1 = 2 + (int)ds.next_bounded((uint32_t)(w - 4));
+    const int d2 = 2 + (int)ds.next_bounded((uint32_t)(h - 4));
+    const int d3 = 2 + (int)ds.next_bounded((uint32_t)(h - 4));
+    uint32_t unused = 0x543210u;  // nibbles: the unused colours in order
+    uint32_t cols = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t j = ds.next_bounded((uint32_t)(6 - k));
+      cols |= ((unused >> (4 * j)) & 15u) << (4 * k);
+      const uint32_t low = unused & ((1u << (4 * j)) - 1u);
+      unused = low | ((unused >> (4 * j + 4)) << (4 * j));  // erase nibble j
+    }
+    g.set(d0, 0, make_cell(K_DOOR_CLOSED, cols & 15));
+    g.set(d1, h - 1, make_cell(K_DOOR_CLOSED, (cols >> 4) & 15));
+    g.set(0, d2, make_cell(K_DOOR_CLOSED, (cols >> 8) & 15));
+    g.set(w - 1, d3, make_cell(K_DOOR_CLOSED, (cols >> 12) & 15));
+    const uint32_t k = ds.next_bounded((uint32_t)((w - 2) * (h - 2)));  // place_agent(size=(w, h))
+    o.ax = 1 + (int)(k % (w - 2));
+    o.ay = 1 + (int)(k / (w - 2));
+    o.dir = (int)ds.next_bounded(4);
+    const uint32_t t = ds.next_bounded(4);
+    const int tx = t == 0 ? d0 : t == 1 ? d1 : t == 2 ? 0 : w - 1;
+    const int ty = t == 0 ? 0 : t == 1 ? h - 1 : t == 2 ? d2 : d3;
+    o.target = (uint32_t)((tx << 4) | ty);
   } else if constexpr (FAM == FAM_CROSSING) {
     // [MG] CrossingEnv._gen_grid, obstacle Wall, N = gparam crossings; the two
     // shuffles as R#35 reads them.  Rivers are nibbles (bit 3: horizontal,

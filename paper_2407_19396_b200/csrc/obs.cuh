@@ -253,6 +253,31 @@ __device__ __forceinline__ void view_columns_wide(const uint64_t* rows, int ax, 
   }
 }
 
+// Out-of-grid view cells as walls ([MG] gen_obs_grid's slice), for grids
+// whose edge is not a closed wall border (GoToDoor, R#37).  Cell vj of
+// column vi lies at lateral offset vi-3 and distance 6-vj from the agent.
+template <int H, int W>
+__device__ __forceinline__ void view_oob_walls(int ax, int ay, int dir, uint32_t (&clo)[7], uint32_t (&chi)[7]) {
+  const int fx = dir == 0 ? 1 : dir == 2 ? -1 : 0, fy = dir == 1 ? 1 : dir == 3 ? -1 : 0;  // forward
+  const int lx = -fy, ly = fx;                                                                // lateral +1
+  uint32_t mlo = 0, mhi = 0;  // bytes along a column that leave the grid (forward component)
+#pragma unroll
+  for (int vj = 0; vj < 7; ++vj) {
+    const int x = ax + (6 - vj) * fx, y = ay + (6 - vj) * fy;
+    const bool out = fx ? (unsigned)x >= (unsigned)W : (unsigned)y >= (unsigned)H;
+    if (vj < 4) mlo |= out ? 0xFFu << (8 * vj) : 0u;
+    else mhi |= out ? 0xFFu << (8 * (vj - 4)) : 0u;
+  }
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    const int x = ax + (vi - 3) * lx, y = ay + (vi - 3) * ly;
+    const bool out = lx ? (unsigned)x >= (unsigned)W : (unsigned)y >= (unsigned)H;
+    const uint32_t m_lo = out ? 0xFFFFFFFFu : mlo, m_hi = out ? 0xFFFFFFFFu : mhi;
+    clo[vi] = (clo[vi] & ~m_lo) | (0x01010101u * CELL_WALL & m_lo);
+    chi[vi] = (chi[vi] & ~m_hi) | (0x01010101u * CELL_WALL & m_hi);
+  }
+}
+
 // Everything after the view columns: opacity, process_vis, encode, emission.
 // out: word-aligned SMEM address at or before this env's record, whose first
 // byte is at misalignment M (warp-uniform, 0..3).  All 7 columns are encoded

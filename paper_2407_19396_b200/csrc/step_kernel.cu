@@ -215,6 +215,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   uint8_t carry = (uint8_t)(rec >> 24);
   uint32_t sc = (uint32_t)((rec >> 32) & 0xFFFF);
   bool prev_done = (rec >> 48) & 1;
+  uint32_t target = FAM == FAM_GOTODOOR ? (uint32_t)(rec >> 56) : 0u;  // GoToDoor target door
 
   float reward = 0.f;
   bool term = false, trunc = false, grid_dirty = false;
@@ -270,6 +271,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     }
     const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi, a.gen_param);
     ax = o.ax; ay = o.ay; dir = o.dir;
+    target = o.target;
     balls = o.balls;
     st_fail = o.fail;
     carry = CELL_EMPTY;
@@ -351,7 +353,9 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       // on the action value.
       sc += 1;
       uint8_t* fp = g.at(fx, fy);
-      const uint32_t fc = *fp;
+      // GoToDoor's grid edge is open: outside the grid reads as a wall (R#37)
+      const bool f_out = FAM == FAM_GOTODOOR && ((unsigned)fx >= (unsigned)W || (unsigned)fy >= (unsigned)H);
+      const uint32_t fc = f_out ? (uint32_t)CELL_WALL : *fp;
       const uint32_t kind = fc & 15u;
       const bool is_fwd = act == 2, is_pick = act == 3, is_drop = act == 4, is_tog = act == 5;
       dir = (dir + (act == 1 ? 1 : 0) + (act == 0 ? 3 : 0)) & 3;
@@ -378,8 +382,18 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       }
       if (FAM == FAM_KEYCORRIDOR && is_pick && (carry & 15) == K_BALL) success = true;  // R#8
       if (FAM == FAM_DYNOBS && is_fwd && not_clear) { coll = true; success = false; }  // R#4
+      bool gtd_end = false;
+      if (FAM == FAM_GOTODOOR) {
+        // [MG] GoToDoorEnv.step: toggle ends the episode; done ends it, a
+        // success iff the agent is next to the target door (R#37)
+        const int tx = (int)(target >> 4), ty = (int)(target & 15);
+        const int ddx = ax - tx, ddy = ay - ty;
+        gtd_end = is_tog || act == 6;
+        success = success || (act == 6 && ddx * ddx + ddy * ddy == 1);
+        coll = gtd_end && !success;  // counted as n_failure, reward 0
+      }
       // ---- a5: reward and termination (Eq. 1, Tables 6-7)
-      if (coll) reward = -1.0f;
+      if (coll && FAM != FAM_GOTODOOR) reward = -1.0f;
       else if (__builtin_expect(success, 0)) reward = success_reward(a.reward_mode, sc, C::T);
       else if (lava) reward = a.reward_mode == 1 ? -1.0f : 0.0f;
       // Code 4 `compose`: + (-time_cost) every step, + (-action_cost) for every
@@ -427,8 +441,11 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
-    if constexpr (RW == 1) observe_emit(lines, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
-    else observe_emit_wide(rows, ax, ay, dir, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
+    uint32_t clo[7], chi[7];
+    if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
+    else view_columns_wide(rows, ax, ay, dir, clo, chi);
+    if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
+    observe_cols(clo, chi, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
 
   EnvResult r;
@@ -439,7 +456,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.trunc = trunc;
   r.dirty = grid_dirty;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48);
+           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)target << 56);
   r.episode = episode;
   r.balls = balls;
   const uint32_t vv = valid ? 1u : 0u;
@@ -829,6 +846,9 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
     case FAM_EMPTY_RANDOM * 10000 + 1616: return launch_fhw<FAM_EMPTY_RANDOM, 16, 16>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT1 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT1, 7, 9>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT2 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT2, 7, 9>(mode, a, n_tiles, s);
+    case FAM_GOTODOOR * 10000 + 505: return launch_fhw<FAM_GOTODOOR, 5, 5>(mode, a, n_tiles, s);
+    case FAM_GOTODOOR * 10000 + 606: return launch_fhw<FAM_GOTODOOR, 6, 6>(mode, a, n_tiles, s);
+    case FAM_GOTODOOR * 10000 + 808: return launch_fhw<FAM_GOTODOOR, 8, 8>(mode, a, n_tiles, s);
     case FAM_CROSSING * 10000 + 909: return launch_fhw<FAM_CROSSING, 9, 9>(mode, a, n_tiles, s);
     case FAM_CROSSING * 10000 + 1111: return launch_fhw<FAM_CROSSING, 11, 11>(mode, a, n_tiles, s);
     default: return cudaErrorInvalidConfiguration;

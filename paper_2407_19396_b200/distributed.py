@@ -68,11 +68,14 @@ def max_over_ranks(x: float, device: torch.device | str = "cpu") -> float:
     return float(t.item())
 
 
-def mean_legacy_return(stats, max_steps: int) -> float:
+def mean_legacy_return(stats, max_steps: int, failure_reward: float = -1.0) -> float:
     """Mean episode return in minigrid reward mode from the reduced statistics
-    (SURVEY §8c-7): (n_success - 0.9 * sum_success_step / T - n_collision) / episodes,
-    evaluated once in binary64 so the reported value is identical for any G."""
+    (SURVEY §8c-7): (n_success - 0.9 * sum_success_step / T + failure_reward *
+    n_failure) / episodes, evaluated once in binary64 so the reported value is
+    identical for any G.  n_failure counts Dynamic-Obstacles collisions
+    (reward -1, the default) and GoToDoor's toggle / done away from the target
+    (reward 0: pass failure_reward=0)."""
     s = [int(v) for v in stats]
     if s[0] == 0:
         return 0.0
-    return (s[2] - 0.9 * s[3] / max_steps - s[5]) / s[0]
+    return (s[2] - 0.9 * s[3] / max_steps + failure_reward * s[5]) / s[0]

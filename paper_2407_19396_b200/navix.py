@@ -21,7 +21,7 @@ _lib = None
 NAVIX_OK, NAVIX_E_UNKNOWN_ENV, NAVIX_E_INVALID_ARG, NAVIX_E_CUDA, NAVIX_E_NOMEM, NAVIX_E_UNSUPPORTED = range(6)
 REWARD_MINIGRID, REWARD_NAVIX = 0, 1
 STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
-                "n_lava", "n_collision", "n_truncated", "gen_failures")
+                "n_lava", "n_failure", "n_truncated", "gen_failures")
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_sample_actions", "navix_step_host", "navix_stats",

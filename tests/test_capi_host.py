@@ -34,6 +34,7 @@ def test_header_symbols_are_exported():
     ("Navix-SimpleCrossingS9N2-v0", 9, 9, 324, 7, 7),
     ("Navix-Crossings-S11N5-v0", 11, 11, 484, 7, 7),
     ("Navix-DoorKey-Random-5x5", 5, 5, 250, 7, 1),
+    ("Navix-GoToDoor-8x8-v0", 8, 8, 256, 7, 8),
 ])
 def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     from oracle import spec_of as oracle_spec

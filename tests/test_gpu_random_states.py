@@ -17,7 +17,7 @@ CASES = [("DoorKey-8x8-v0", 0), ("Empty-5x5-v0", 0), ("LavaGapS7-v0", 0), ("KeyC
          ("Dynamic-Obstacles-8x8-v0", 4), ("KeyCorridorS3R1-v0", 0), ("DoorKey-6x6-v0", 0),
          ("Dynamic-Obstacles-5x5-v0", 2), ("DoorKey-16x16-v0", 0), ("Dynamic-Obstacles-16x16-v0", 8),
          ("KeyCorridorS5R3-v0", 0), ("DistShift2-v0", 0), ("Empty-Random-6x6-v0", 0),
-         ("SimpleCrossingS11N5-v0", 0)]
+         ("SimpleCrossingS11N5-v0", 0), ("GoToDoor-5x5-v0", 0), ("GoToDoor-8x8-v0", 0)]
 
 
 @pytest.mark.parametrize("env_id,nob", CASES)
@@ -27,7 +27,8 @@ def test_random_states_observe_and_step(env_id, nob):
     g = NavixEnv(env_id, n, seed=21)
     s = g.spec
     o = OracleEnv(env_id, n, seed=21)
-    recs = random_records(zlib.crc32(env_id.encode()) % 1000, n, s.height, s.width, s.max_steps, nob, p_prev_done=0.05)
+    recs = random_records(zlib.crc32(env_id.encode()) % 1000, n, s.height, s.width, s.max_steps, nob, p_prev_done=0.05,
+                          open_edge=env_id.startswith("GoToDoor"))  # R#37: open grid edge, target bytes
     g.import_state(recs)
     o.import_(recs)
     np.testing.assert_array_equal(g.export_state(), recs)  # import/export round trip

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 from scipy import stats as sps
 
+from inputgen import record_from_map
 from oracle import OracleEnv, spec_of
 
 R, L, F = 1, 0, 2  # right, left, forward
@@ -98,7 +99,7 @@ def test_empty_random_start_is_uniform(S):
 
 def test_empty_random_goal_reward_from_known_start():
     # import a start next to the goal and step onto it: success reward with T = 4 S^2
-    from inputgen import record_from_map
+
     m = ["######",
          "#....#",
          "#....#",
@@ -184,3 +185,133 @@ def test_crossing_river_subset_and_opening_uniform():
                 ys.append(1 + int(np.argmax(col != 2)))
     c = np.bincount(ys, minlength=8)[1:]
     assert len(ys) > 3000 and sps.chisquare(c).pvalue > 1e-4
+
+
+# ---------------------------------------------------------------- GoToDoor
+def _gtd(S, n, seed=3):
+    env = OracleEnv(f"GoToDoor-{S}x{S}-v0", n, seed=seed)
+    env.reset()
+    return env, env.observe_full(), env.export()
+
+
+@pytest.mark.parametrize("S", [5, 6, 8])
+def test_gotodoor_structure(S):
+    s = spec_of(f"GoToDoor-{S}x{S}-v0")
+    assert (s.width, s.height, s.max_steps, s.n_actions, s.export_bytes) == (S, S, 4 * S * S, 7, 3 * S * S + 14)
+    n = 3000
+    _, full, rec = _gtd(S, n)
+    ws, hs, tgt_side, first_col = [], [], [], []
+    for k in range(n):
+        t, c, st = full[k, :, :, 0], full[k, :, :, 1], full[k, :, :, 2]
+        # room: the wall rectangle from (0,0); its size from the top wall's extent
+        w = 1 + max(x for x in range(S) if t[x, 0] in (2, 4))
+        h = 1 + max(y for y in range(S) if t[0, y] in (2, 4))
+        assert 5 <= w <= S and 5 <= h <= S
+        ring = [(x, 0) for x in range(w)] + [(x, h - 1) for x in range(w)] + \
+               [(0, y) for y in range(1, h - 1)] + [(w - 1, y) for y in range(1, h - 1)]
+        doors = [(x, y) for (x, y) in ring if t[x, y] == 4]
+        assert len(doors) == 4 and all(t[x, y] == 2 for (x, y) in ring if (x, y) not in doors)
+        assert all(st[x, y] == 1 for x, y in doors)                  # closed, not locked
+        cols = [int(c[x, y]) for x, y in doors]
+        assert len(set(cols)) == 4                                   # distinct colours
+        top = [d for d in doors if d[1] == 0 and 0 < d[0] < w - 1]
+        bot = [d for d in doors if d[1] == h - 1 and 0 < d[0] < w - 1]
+        lef = [d for d in doors if d[0] == 0]
+        rig = [d for d in doors if d[0] == w - 1]
+        assert len(top) == len(bot) == len(lef) == len(rig) == 1
+        assert 2 <= top[0][0] <= w - 3 and 2 <= bot[0][0] <= w - 3
+        assert 2 <= lef[0][1] <= h - 3 and 2 <= rig[0][1] <= h - 3
+        # everything outside the room is empty, the inside is empty but the agent
+        out = np.ones((S, S), bool)
+        out[:w, :h] = False
+        assert np.all(t[out] == 1)
+        ag = np.argwhere(t == 10)
+        assert len(ag) == 1 and 1 <= ag[0][0] <= w - 2 and 1 <= ag[0][1] <= h - 2
+        tx, ty = int(rec[k, -2]), int(rec[k, -1])
+        assert (tx, ty) in doors
+        ws.append(w)
+        hs.append(h)
+        tgt_side.append([top[0], bot[0], lef[0], rig[0]].index((tx, ty)))
+        first_col.append(int(c[top[0]]))
+    if S == 5:
+        assert set(ws) == set(hs) == {5}
+    else:
+        assert sps.chisquare(np.bincount(ws, minlength=S + 1)[5:]).pvalue > 1e-4
+        assert sps.chisquare(np.bincount(hs, minlength=S + 1)[5:]).pvalue > 1e-4
+    assert sps.chisquare(np.bincount(tgt_side, minlength=4)).pvalue > 1e-4
+    assert sps.chisquare(np.bincount(first_col, minlength=6)).pvalue > 1e-4
+
+
+ROOM5 = ["##D##",
+         "#...#",
+         "D.A.D",
+         "#...#",
+         "##D##"]
+
+
+def _room(action_seq, agent_dir, target, S=5, rows=ROOM5, reward_mode=0):
+    env = OracleEnv(f"GoToDoor-{S}x{S}-v0", 1, reward_mode=reward_mode)
+    env.reset()
+    env.import_(record_from_map(rows, agent_dir, target=target).reshape(1, -1))
+    outs = []
+    for a in action_seq:
+        o, r, te, tr = env.step(np.array([a], np.uint8))
+        outs.append((o[0], float(r[0]), int(te[0]), int(tr[0])))
+    return env, outs
+
+
+def test_gotodoor_done_next_to_target_succeeds():
+    # agent (2,2) facing north; target the top door (2,0): forward to (2,1), done
+    env, outs = _room([F, 6], 3, (2, 0))
+    assert outs[0][1:] == (0.0, 0, 0)
+    assert outs[1][2] == 1 and outs[1][1] == pytest.approx(1 - 0.9 * 2 / 100, abs=1e-7)
+    st = env.stats()
+    assert st[0] == 1 and st[2] == 1 and st[5] == 0
+    # navix reward mode: 1
+    _, outs = _room([F, 6], 3, (2, 0), reward_mode=1)
+    assert outs[1][1:3] == (1.0, 1)
+
+
+def test_gotodoor_done_elsewhere_and_toggle_fail():
+    env, outs = _room([F, 6], 3, (0, 2))   # next to the top door, but the target is the left one
+    assert outs[1][1:] == (0.0, 1, 0)
+    assert env.stats()[5] == 1             # n_failure
+    env, outs = _room([6], 3, (2, 0))      # (2,2) is 2 cells from the target: not adjacent
+    assert outs[0][1:] == (0.0, 1, 0)
+    # toggle ends the episode (the door it faces is opened first)
+    env, outs = _room([F, 5], 3, (2, 0))
+    assert outs[1][1:] == (0.0, 1, 0)
+    assert env.stats()[5] == 1
+    full = env.observe_full()[0]
+    assert full[2, 0].tolist() == [4, 4, 0]   # the top door is open now
+
+
+def test_gotodoor_open_door_on_the_grid_edge_sees_outside_as_wall():
+    # after toggling the top door open from (2,1) facing north, the view runs
+    # off the grid: [MG] slices out-of-grid cells as Walls, so the cell behind
+    # the door is a visible wall and everything further is unseen; the open
+    # door's own row-4 neighbours (i +- 1, j - 1) are lit by process_vis too
+    _, outs = _room([F, 5], 3, (4, 2))
+    obs = outs[1][0]                              # [vi][vj][c], agent at (3, 6)
+    assert obs[3, 6].tolist() == [1, 0, 0]        # own cell (carrying nothing)
+    assert obs[3, 5].tolist() == [4, 4, 0]        # the open door in front
+    assert obs[3, 4].tolist() == [2, 5, 0]        # outside the grid: wall
+    assert obs[3, 3].tolist() == [0, 0, 0]        # behind it: unseen
+    assert obs[2, 4].tolist() == obs[4, 4].tolist() == [2, 5, 0]
+    assert np.count_nonzero(obs[:, :5, 0]) == 3   # rows beyond the door: only those walls
+
+
+def test_gotodoor_open_edge_walk_blocked_outside():
+    # an imported GoToDoor state may have an open grid edge (R#37): walking
+    # off the grid is blocked as if by a wall
+    rows = ["..D..",
+            ".....",
+            "A....",
+            ".....",
+            "....."]
+    env = OracleEnv("GoToDoor-5x5-v0", 1)
+    env.reset()
+    env.import_(record_from_map(rows, 2, target=(2, 0)).reshape(1, -1))  # facing west at x = 0
+    _, r, te, _ = env.step(np.array([F], np.uint8))
+    rec = env.export()[0]
+    assert (rec[75], rec[76]) == (0, 2) and te[0] == 0

@@ -85,7 +85,7 @@ def test_p2c_dynobs_wall_collision_any_seed():
             for e in range(4):
                 d = decode_record(rec[e], 8, 8, 4)
                 assert d["agent"][:2] == (1, 1)
-            assert env.stats()[5] == 4  # n_collision
+            assert env.stats()[5] == 4  # n_failure (collisions)
 
 
 LAVA_MAP = ["#######",
