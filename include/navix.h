@@ -64,7 +64,8 @@ enum {
   NAVIX_FAMILY_EMPTY_RANDOM = 5,
   NAVIX_FAMILY_DISTSHIFT = 6,
   NAVIX_FAMILY_CROSSING = 7,
-  NAVIX_FAMILY_GOTODOOR = 8
+  NAVIX_FAMILY_GOTODOOR = 8,
+  NAVIX_FAMILY_FOURROOMS = 9
 };
 
 /* Reward modes (R#1/R#3): MINIGRID = legacy 1 - 0.9*sc/T on success,

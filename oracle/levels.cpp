@@ -182,6 +182,42 @@ static void gen_crossing(Env& e, DrawStream& ds) {
   }
 }
 
+// ---------------------------------------------------------------- FourRooms
+// [MG] FourRoomsEnv._gen_grid, step by step: outer walls; for each room
+// (j outer, i inner) its right wall with one opening, then its bottom wall
+// with one opening; place_agent() over the whole grid, then place_obj(Goal).
+static void gen_fourrooms(Env& e, DrawStream& ds) {
+  const int W = e.spec.width, H = e.spec.height;
+  e.grid = Grid(W, H);
+  e.grid.horz_wall(0, 0, -1, make_wall());
+  e.grid.horz_wall(0, H - 1, -1, make_wall());
+  e.grid.vert_wall(0, 0, -1, make_wall());
+  e.grid.vert_wall(W - 1, 0, -1, make_wall());
+  const int room_w = W / 2, room_h = H / 2;
+  for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 2; ++i) {
+      const int xL = i * room_w, yT = j * room_h, xR = xL + room_w, yB = yT + room_h;
+      if (i + 1 < 2) {
+        e.grid.vert_wall(xR, yT, room_h, make_wall());
+        const int y = yT + 1 + (int)ds.next_bounded((uint32_t)(yB - yT - 1));  // _rand_int(yT + 1, yB)
+        e.grid.set(xR, y, Cell());
+      }
+      if (j + 1 < 2) {
+        e.grid.horz_wall(xL, yB, room_w, make_wall());
+        const int x = xL + 1 + (int)ds.next_bounded((uint32_t)(xR - xL - 1));  // _rand_int(xL + 1, xR)
+        e.grid.set(x, yB, Cell());
+      }
+    }
+  e.agent_x = -1; e.agent_y = -1;
+  int ax, ay;
+  place_uniform(e, 0, 0, W, H, ds.next(), nullptr, &ax, &ay);
+  e.agent_x = ax; e.agent_y = ay;
+  e.agent_dir = (int)ds.next_bounded(4);
+  int gx, gy;
+  place_uniform(e, 0, 0, W, H, ds.next(), nullptr, &gx, &gy);
+  e.grid.set(gx, gy, make_goal());
+}
+
 // ---------------------------------------------------------------- GoToDoor
 // [MG] GoToDoorEnv._gen_grid, step by step.  _rand_int(a, b) = a +
 // bounded(draw, b - a); the colour loop (rand_elem until unused) is one draw
@@ -459,6 +495,7 @@ void Env::generate() {
     case F_DISTSHIFT: gen_distshift(*this); break;
     case F_CROSSING: gen_crossing(*this, ds); break;
     case F_GOTODOOR: gen_gotodoor(*this, ds); break;
+    case F_FOURROOMS: gen_fourrooms(*this, ds); break;
   }
   step_count = 0;
   prev_done = false;

@@ -215,6 +215,13 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     s.n_crossings = N;
     s.max_steps = 4 * S * S;  // [MG] CrossingEnv
     s.n_actions = 7;
+  } else if (id == "FourRooms") {
+    // [MG] FourRoomsEnv at Table 9's 17x17 (MG's default is 19), max_steps 100 (R#38)
+    s.family = F_FOURROOMS;
+    s.size = 17;
+    s.height = s.width = 17;
+    s.max_steps = 100;
+    s.n_actions = 7;
   } else if (square("GoToDoor-", F_GOTODOOR)) {
     // [MG] GoToDoorEnv(size): a random room of 5..size cells per side, 4 doors
     if (s.size < 5 || s.size > 16) return false;

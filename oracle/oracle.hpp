@@ -35,7 +35,8 @@ enum : int { A_LEFT = 0, A_RIGHT = 1, A_FORWARD = 2, A_PICKUP = 3, A_DROP = 4, A
 
 // Families of Table 9 implemented by the oracle.
 enum Family : int { F_EMPTY = 0, F_DOORKEY = 1, F_DYNOBS = 2, F_KEYCORRIDOR = 3, F_LAVAGAP = 4, F_EMPTY_RANDOM = 5,
-                    F_DISTSHIFT = 6, F_CROSSING = 7, F_GOTODOOR = 8 };
+                    F_DISTSHIFT = 6, F_CROSSING = 7, F_GOTODOOR = 8,
+                    F_FOURROOMS = 9 };
 
 // One MiniGrid WorldObj.  `tag` is test-only bookkeeping (rotation pin P6).
 struct Obj {

@@ -93,6 +93,8 @@ int parse_id(const char* env_id, EnvConfig* c) {
              sscanf(id.c_str(), "Crossings-S%dN%d%c", &a, &b, &tail) == 2) {  // [MG] CrossingEnv (R#35)
     if (!((a == 9 && b >= 1 && b <= 3) || (a == 11 && b == 5))) return 1;
     *c = EnvConfig{FAM_CROSSING, a, a, 4 * a * a, 7, 0, 0, 0, b};
+  } else if (id == "FourRooms") {  // [MG] FourRoomsEnv at Table 9's 17x17, max_steps 100 (R#38)
+    *c = EnvConfig{FAM_FOURROOMS, 17, 17, 100, 7, 0, 0, 0};
   } else if (sq("GoToDoor-%dx%d%c")) {  // [MG] GoToDoorEnv (R#37)
     if (a != 5 && a != 6 && a != 8) return 1;
     *c = EnvConfig{FAM_GOTODOOR, a, a, 4 * a * a, 7, 0, 0, 0};
@@ -115,7 +117,7 @@ int parse_id(const char* env_id, EnvConfig* c) {
   } else {
     return 1;
   }
-  return (c->height <= 16 && c->width <= 16) ? 0 : 2;
+  return (c->height <= 24 && c->width <= 24) ? 0 : 2;
 }
 
 void fill_spec(const EnvConfig& c, navix_spec* s) {
@@ -126,7 +128,8 @@ void fill_spec(const EnvConfig& c, navix_spec* s) {
   s->max_steps = c.max_steps;
   s->obs_bytes = OBS_BYTES;
   // public NAVIX_FAMILY_* ids: DistShift1/2 share one, SimpleCrossing is 7
-  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family == FAM_CROSSING ? 7 : c.family == FAM_GOTODOOR ? 8 : c.family;
+  s->family = c.family == FAM_DISTSHIFT2 ? FAM_DISTSHIFT1 : c.family == FAM_CROSSING ? 7 : c.family == FAM_GOTODOOR ? 8
+              : c.family == FAM_FOURROOMS ? 9 : c.family;
   s->n_obstacles = c.n_obstacles;
   s->export_bytes = 3 * c.height * c.width + 12 + 2 * c.n_obstacles + (c.family == FAM_GOTODOOR ? 2 : 0);
 }
@@ -423,7 +426,7 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
   uint8_t* o = static_cast<uint8_t*>(host);
   for (int64_t i = 0; i < h->n; ++i) {
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
-    uint8_t cells[16][16];
+    uint8_t cells[24][24];
     for (int y = 0; y < c.height; ++y)
       for (int x = 0; x < c.width; ++x)
         cells[y][x] = (uint8_t)(grid[(size_t)(tile * HP + y * RW + x / 8) * TILE + lane] >> (8 * (x % 8)));
@@ -474,7 +477,7 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
   const uint8_t* in = static_cast<const uint8_t*>(host);
   for (int64_t i = 0; i < h->n; ++i) {
     const uint8_t* p = in + (size_t)i * per;
-    uint8_t cells[16][16] = {};
+    uint8_t cells[24][24] = {};
     for (int y = 0; y < H; ++y)
       for (int x = 0; x < W; ++x, p += 3) {
         if (!to_cell(p, &cells[y][x]))

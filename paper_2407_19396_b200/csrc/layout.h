@@ -53,7 +53,7 @@ constexpr uint8_t CELL_LAVA = make_cell(K_LAVA, COL_RED);
 
 enum Family : int { FAM_EMPTY = 0, FAM_DOORKEY = 1, FAM_DYNOBS = 2, FAM_KEYCORRIDOR = 3, FAM_LAVAGAP = 4,
                     FAM_EMPTY_RANDOM = 5, FAM_DISTSHIFT1 = 6, FAM_DISTSHIFT2 = 7, FAM_CROSSING = 8,
-                    FAM_GOTODOOR = 9 };
+                    FAM_GOTODOOR = 9, FAM_FOURROOMS = 10 };
 
 struct EnvConfig {
   int family;
@@ -74,7 +74,7 @@ struct StateLayout {
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // u64 planes per grid row: 8-byte rows up to width 8, 16-byte rows up to 16 (row f2)
-__host__ __device__ constexpr int row_planes(int width) { return width > 8 ? 2 : 1; }
+__host__ __device__ constexpr int row_planes(int width) { return (width + 7) / 8; }
 
 inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   StateLayout L{};

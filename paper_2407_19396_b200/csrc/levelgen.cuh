@@ -13,12 +13,13 @@ namespace navix {
 // Compile-time configuration of one kernel instantiation.
 template <int FAM, int H, int W>
 struct Cfg {
-  static constexpr int RW = W > 8 ? 2 : 1;           // u64 planes per grid row (f2: 16-byte rows)
-  static constexpr int NPL = RW == 1 ? 8 : 32;       // SMEM planes per env (8 lines / 16 rows x 2)
+  static constexpr int RW = (W + 7) / 8;             // u64 planes per grid row (f2: 16- / 24-byte rows)
+  static constexpr int NPL = RW == 1 ? 8 : RW == 2 ? 32 : RW * H;  // SMEM planes per env (8 lines / 16 rows x 2 / H x RW)
   static constexpr int RS = (W - 1) / 3 + 1;         // KeyCorridor room size (3 columns of rooms)
   static constexpr int NR = (H - 1) / (RS - 1);      // KeyCorridor rows
   static constexpr int T = FAM == FAM_DOORKEY ? 10 * W * W
                          : FAM == FAM_KEYCORRIDOR ? 30 * RS * RS
+                         : FAM == FAM_FOURROOMS ? 100
                          : 4 * W * H;                // R#16
   static constexpr int NA = FAM == FAM_DYNOBS ? 3 : 7;
   static constexpr int NOBST = FAM != FAM_DYNOBS ? 0 : (W == 5 ? 2 : W == 6 ? 3 : W == 16 ? 8 : 4);  // R#6
@@ -28,7 +29,7 @@ struct Cfg {
 // cell bytes (cells x >= W are 0 = outside the grid).
 template <int FAM, int H, int W>
 __host__ __device__ constexpr uint64_t template_plane(int p) {
-  constexpr int RW = W > 8 ? 2 : 1;
+  constexpr int RW = (W + 7) / 8;
   const int y = p / RW, x0 = 8 * (p % RW);
   uint64_t r = 0;
   for (int x = x0; x < x0 + 8 && x < W; ++x) {
@@ -42,6 +43,8 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
       const int strip2 = FAM == FAM_DISTSHIFT1 ? 2 : 5;
       if (x == W - 2 && y == 1) c = CELL_GOAL;
       if (x >= 3 && x < W - 3 && (y == 1 || y == strip2)) c = CELL_LAVA;
+    } else if (FAM == FAM_FOURROOMS) {
+      if (x == W / 2 || y == H / 2) c = CELL_WALL;  // the inner walls; the generator opens 4 gaps
     } else if (FAM != FAM_KEYCORRIDOR && FAM != FAM_GOTODOOR && x == W - 2 && y == H - 2) {
       c = CELL_GOAL;  // goal (W-2, H-2)
     }
@@ -119,6 +122,41 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     o.ax = 1 + (int)(k % (W - 2));
     o.ay = 1 + (int)(k / (W - 2));
     o.dir = (int)ds.next_bounded(4);
+  } else if constexpr (FAM == FAM_FOURROOMS) {
+    // [MG] FourRoomsEnv._gen_grid (R#38): one opening per inner wall segment
+    // in [MG]'s order (right wall of room (0,0), bottom of (0,0), bottom of
+    // (1,0), right of (0,1)); then place_agent() and place_obj(Goal) over the
+    // whole grid, uniform over the empty cells in row-major order
+    constexpr int RX = W / 2, RY = H / 2;
+    const int o0 = 1 + (int)ds.next_bounded(RY - 1);               // (RX, o0)
+    const int o1 = 1 + (int)ds.next_bounded(RX - 1);               // (o1, RY)
+    const int o2 = RX + 1 + (int)ds.next_bounded(W - 1 - RX - 1);  // (o2, RY)
+    const int o3 = RY + 1 + (int)ds.next_bounded(H - 1 - RY - 1);  // (RX, o3)
+    g.set(RX, o0, CELL_EMPTY);
+    g.set(o1, RY, CELL_EMPTY);
+    g.set(o2, RY, CELL_EMPTY);
+    g.set(RX, o3, CELL_EMPTY);
+    // empty cells of row y as a bit mask over x
+    constexpr uint32_t inner = ((1u << (W - 1)) - 1u) & ~1u;
+    auto row_free = [&](int y) -> uint32_t {
+      if (y == RY) return (1u << o1) | (1u << o2);
+      return (y == o0 || y == o3) ? inner : inner & ~(1u << RX);
+    };
+    auto pick = [&](uint32_t k, int skip_x, int skip_y, int& px, int& py) {
+      for (int y = 1; y < H - 1; ++y) {
+        uint32_t m = row_free(y);
+        if (y == skip_y) m &= ~(1u << skip_x);
+        const uint32_t c = __popc(m);
+        if (k < c) { px = select64(m, k); py = y; return; }
+        k -= c;
+      }
+    };
+    const uint32_t nfree = (uint32_t)((H - 2) * (W - 2) - (W - 2) - (H - 2) + 1 + 4);
+    pick(ds.next_bounded(nfree), -1, -1, o.ax, o.ay);
+    o.dir = (int)ds.next_bounded(4);
+    int gx = 0, gy = 0;
+    pick(ds.next_bounded(nfree - 1), o.ax, o.ay, gx, gy);
+    g.set(gx, gy, CELL_GOAL);
   } else if constexpr (FAM == FAM_GOTODOOR) {
     // [MG] GoToDoorEnv._gen_grid: room size, walls, 4 door positions, 4
     // distinct colours (one draw over the unused ones, R#37), agent, target

@@ -253,6 +253,53 @@ __device__ __forceinline__ void view_columns_wide(const uint64_t* rows, int ax, 
   }
 }
 
+// The same for rows of RW >= 3 planes (grids wider than 16, FourRooms): row
+// y is clamped into the grid and the window is read from the row with 8 zero
+// bytes prepended (virtual word w < 2 is 0), so every load stays inside this
+// env's H x RW planes; out-of-grid positions read arbitrary bytes (R#12).
+template <int RW, int H>
+__device__ __forceinline__ uint32_t row_word_v(const uint64_t* rows, int y, int w) {
+  const int yc = y < 0 ? 0 : y >= H ? H - 1 : y;
+  const int wc = w < 2 ? 2 : w > 2 * RW + 1 ? 2 * RW + 1 : w;
+  const uint32_t v = reinterpret_cast<const uint32_t*>(rows + (yc * RW + ((wc - 2) >> 1)) * TILE)[wc & 1];
+  return w < 2 ? 0u : v;
+}
+template <int RW, int H>
+__device__ __forceinline__ void view_columns_big(const uint64_t* rows, int ax, int ay, int dir, uint32_t (&clo)[7],
+                                                 uint32_t (&chi)[7]) {
+  const int base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
+  const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
+  const int s = dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6;  // first position of the window
+  const bool rev = dir <= 1;
+  if ((dir & 1) == 0) {
+    const int sv = s + 8, q = sv >> 2, r = 8 * (sv & 3);  // virtual byte offset (>= 2 for ax >= 0)
+#pragma unroll
+    for (int vi = 0; vi < 7; ++vi) {
+      const int y = base + sgn * vi;
+      const uint32_t w0 = row_word_v<RW, H>(rows, y, q), w1 = row_word_v<RW, H>(rows, y, q + 1),
+                     w2 = row_word_v<RW, H>(rows, y, q + 2);
+      const uint32_t f_lo = __funnelshift_r(w0, w1, r), f_hi = __funnelshift_r(w1, w2, r);
+      clo[vi] = rev ? prmt(f_lo, f_hi, 0x3456u) : f_lo;
+      chi[vi] = rev ? prmt(f_lo, f_hi, 0x0012u) : f_hi;
+    }
+  } else {
+#pragma unroll
+    for (int vi = 0; vi < 7; ++vi) {
+      int x = base + sgn * vi;
+      x = x < 0 ? 0 : x > 8 * RW - 1 ? 8 * RW - 1 : x;
+      const uint32_t xb = (uint32_t)(x & 3), pair = ((4u + xb) << 4) | xb;
+      uint32_t w[7];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) w[k] = row_word_v<RW, H>(rows, s + k, (x >> 2) + 2);  // rows s .. s+6, byte x
+      const uint32_t p01 = prmt(w[0], w[1], pair), p23 = prmt(w[2], w[3], pair);
+      const uint32_t p45 = prmt(w[4], w[5], pair), p6 = prmt(w[6], w[6], pair);
+      const uint32_t f_lo = prmt(p01, p23, 0x5410u), f_hi = prmt(p45, p6, 0x5410u);  // cells y = s .. s+6
+      clo[vi] = rev ? prmt(f_lo, f_hi, 0x3456u) : f_lo;
+      chi[vi] = rev ? prmt(f_lo, f_hi, 0x0012u) : f_hi;
+    }
+  }
+}
+
 // Out-of-grid view cells as walls ([MG] gen_obs_grid's slice), for grids
 // whose edge is not a closed wall border (GoToDoor, R#37).  Cell vj of
 // column vi lies at lateral offset vi-3 and distance 6-vj from the agent.

@@ -443,7 +443,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
     uint32_t clo[7], chi[7];
     if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
-    else view_columns_wide(rows, ax, ay, dir, clo, chi);
+    else if constexpr (RW == 2) view_columns_wide(rows, ax, ay, dir, clo, chi);
+    else view_columns_big<RW, H>(rows, ax, ay, dir, clo, chi);
     if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
     observe_cols(clo, chi, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
   }
@@ -846,6 +847,7 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
     case FAM_EMPTY_RANDOM * 10000 + 1616: return launch_fhw<FAM_EMPTY_RANDOM, 16, 16>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT1 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT1, 7, 9>(mode, a, n_tiles, s);
     case FAM_DISTSHIFT2 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT2, 7, 9>(mode, a, n_tiles, s);
+    case FAM_FOURROOMS * 10000 + 1717: return launch_fhw<FAM_FOURROOMS, 17, 17>(mode, a, n_tiles, s);
     case FAM_GOTODOOR * 10000 + 505: return launch_fhw<FAM_GOTODOOR, 5, 5>(mode, a, n_tiles, s);
     case FAM_GOTODOOR * 10000 + 606: return launch_fhw<FAM_GOTODOOR, 6, 6>(mode, a, n_tiles, s);
     case FAM_GOTODOOR * 10000 + 808: return launch_fhw<FAM_GOTODOOR, 8, 8>(mode, a, n_tiles, s);

@@ -35,6 +35,7 @@ def test_header_symbols_are_exported():
     ("Navix-Crossings-S11N5-v0", 11, 11, 484, 7, 7),
     ("Navix-DoorKey-Random-5x5", 5, 5, 250, 7, 1),
     ("Navix-GoToDoor-8x8-v0", 8, 8, 256, 7, 8),
+    ("Navix-FourRooms-v0", 17, 17, 100, 7, 9),
 ])
 def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     from oracle import spec_of as oracle_spec

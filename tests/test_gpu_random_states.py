@@ -17,7 +17,8 @@ CASES = [("DoorKey-8x8-v0", 0), ("Empty-5x5-v0", 0), ("LavaGapS7-v0", 0), ("KeyC
          ("Dynamic-Obstacles-8x8-v0", 4), ("KeyCorridorS3R1-v0", 0), ("DoorKey-6x6-v0", 0),
          ("Dynamic-Obstacles-5x5-v0", 2), ("DoorKey-16x16-v0", 0), ("Dynamic-Obstacles-16x16-v0", 8),
          ("KeyCorridorS5R3-v0", 0), ("DistShift2-v0", 0), ("Empty-Random-6x6-v0", 0),
-         ("SimpleCrossingS11N5-v0", 0), ("GoToDoor-5x5-v0", 0), ("GoToDoor-8x8-v0", 0)]
+         ("SimpleCrossingS11N5-v0", 0), ("GoToDoor-5x5-v0", 0), ("GoToDoor-8x8-v0", 0),
+         ("FourRooms-v0", 0)]
 
 
 @pytest.mark.parametrize("env_id,nob", CASES)

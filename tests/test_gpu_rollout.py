@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
     ("LavaGapS7-v0", 513, 120), ("Empty-5x5-v0", 16, 250), ("DoorKey-5x5-v0", 129, 64),
     ("KeyCorridorS3R1-v0", 200, 290), ("DoorKey-16x16-v0", 300, 100), ("Dynamic-Obstacles-16x16-v0", 260, 60),
     ("Empty-Random-6x6-v0", 300, 150), ("DistShift1-v0", 300, 120),
-    ("SimpleCrossingS9N3-v0", 300, 150), ("GoToDoor-8x8-v0", 300, 100)])
+    ("SimpleCrossingS9N3-v0", 300, 150), ("GoToDoor-8x8-v0", 300, 100),
+    ("FourRooms-v0", 300, 130)])
 def test_rollout_equals_sequential_steps(env_id, n, K):
     from paper_2407_19396_b200 import NavixEnv
     a = NavixEnv(env_id, n, seed=8)

@@ -39,7 +39,8 @@ def test_reward_costs_parity(env_id, mode):
 @pytest.mark.parametrize("env_id,nob", [("DoorKey-8x8-v0", 0), ("KeyCorridorS3R3-v0", 0),
                                         ("Dynamic-Obstacles-8x8-v0", 4), ("Empty-5x5-v0", 0),
                                         ("KeyCorridorS3R1-v0", 0), ("LavaGapS6-v0", 0),
-                                        ("DoorKey-16x16-v0", 0), ("Dynamic-Obstacles-16x16-v0", 8)])
+                                        ("DoorKey-16x16-v0", 0), ("Dynamic-Obstacles-16x16-v0", 8),
+                                        ("FourRooms-v0", 0)])
 def test_full_obs_parity(env_id, nob):
     from paper_2407_19396_b200 import NavixEnv
     n = 1500

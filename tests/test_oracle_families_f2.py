@@ -315,3 +315,56 @@ def test_gotodoor_open_edge_walk_blocked_outside():
     _, r, te, _ = env.step(np.array([F], np.uint8))
     rec = env.export()[0]
     assert (rec[75], rec[76]) == (0, 2) and te[0] == 0
+
+
+# ---------------------------------------------------------------- FourRooms
+def test_fourrooms_structure_and_uniform_placement():
+    s = spec_of("Navix-FourRooms-v0")
+    assert (s.width, s.height, s.max_steps, s.n_actions) == (17, 17, 100, 7)   # Table 9 size, [MG] T (R#38)
+    n = 20000
+    env = OracleEnv("FourRooms-v0", n, seed=2)
+    env.reset()
+    full = env.observe_full()
+    t = full[:, :, :, 0]
+    ag_cells, goal_cells, gaps = [], [], []
+    for k in range(0, n):
+        tk = t[k]
+        border = np.ones((17, 17), bool)
+        border[1:-1, 1:-1] = False
+        assert np.all(tk[border] == 2)
+        if k < 300:
+            segs = {"v_top": [(8, y) for y in range(1, 8)], "v_bot": [(8, y) for y in range(9, 16)],
+                    "h_left": [(x, 8) for x in range(1, 8)], "h_right": [(x, 8) for x in range(9, 16)]}
+            for cells in segs.values():
+                assert sum(tk[c] != 2 for c in cells) == 1     # exactly one opening per segment
+            assert tk[8, 8] == 2
+            inner = tk[1:-1, 1:-1]
+            walls = np.count_nonzero(inner == 2)
+            assert walls == 15 + 15 - 1 - 4
+            # every free cell is reachable from the agent
+            seen = _reachable(np.where(tk == 2, 2, 1), *np.argwhere(tk == 10)[0])
+            assert np.all(seen[tk != 2])
+            gaps.append([c for cells in segs.values() for c in cells if tk[c] != 2])
+        (ax, ay), = np.argwhere(tk == 10)
+        (gx, gy), = np.argwhere(tk == 8)
+        ag_cells.append((ax, ay))
+        goal_cells.append((gx, gy))
+    # agent and goal uniform over the 200 free cells (cells are free in the
+    # rooms' interiors; wall rows/columns only through their openings)
+    room = [(x, y) for y in range(1, 16) for x in range(1, 16) if x != 8 and y != 8]
+    idx = {c: i for i, c in enumerate(room)}
+    a = np.bincount([idx[c] for c in ag_cells if c in idx], minlength=len(room))
+    g = np.bincount([idx[c] for c in goal_cells if c in idx], minlength=len(room))
+    assert sps.chisquare(a).pvalue > 1e-4 and sps.chisquare(g).pvalue > 1e-4
+    assert all(a_ != g_ for a_, g_ in zip(ag_cells, goal_cells))
+
+
+def test_fourrooms_truncates_at_100():
+    env = OracleEnv("FourRooms-v0", 4, seed=1)
+    env.reset()
+    for t in range(100):
+        _, r, te, tr = env.step(np.zeros(4, np.uint8))   # turning left forever
+        assert not te.any()
+        assert tr.all() == (t == 99)
+    _, r, te, tr = env.step(np.zeros(4, np.uint8))
+    assert env.export()[:, 3 * 289 + 5].tolist() == [0, 0, 0, 0]  # auto-reset: step_count 0
