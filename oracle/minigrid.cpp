@@ -412,7 +412,16 @@ StepOut Env::step(int action) {
       break;
   }
   bool failure = false;
-  if (S.family == F_GOTODOOR) {
+  if (S.family == F_GOTODOOR && reward_mode == RM_NAVIX) {
+    // Table 6 / Table 7 `on_door_done`: +1 and termination when
+    // done is performed in front of the mission's door; nothing else ends the
+    // episode (R#39)
+    if (action == A_DONE && fp.first == target_x && fp.second == target_y) {
+      reward = success_reward(reward_mode, step_count, S.max_steps);
+      success = true;
+      terminated = true;
+    }
+  } else if (S.family == F_GOTODOOR) {
     // [MG] GoToDoorEnv.step: toggle ends the episode (the door is already
     // toggled); done ends it, with the success reward iff the agent is next
     // to the target door (R#37)

@@ -385,11 +385,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       bool gtd_end = false;
       if (FAM == FAM_GOTODOOR) {
         // [MG] GoToDoorEnv.step: toggle ends the episode; done ends it, a
-        // success iff the agent is next to the target door (R#37)
+        // success iff the agent is next to the target door (R#37).  Navix
+        // reward mode: Table 6/7 `on_door_done`, done in front of the target
+        // door is the only event (R#39)
         const int tx = (int)(target >> 4), ty = (int)(target & 15);
         const int ddx = ax - tx, ddy = ay - ty;
-        gtd_end = is_tog || act == 6;
-        success = success || (act == 6 && ddx * ddx + ddy * ddy == 1);
+        const bool nav = a.reward_mode == 1;
+        const bool hit = nav ? (fx == tx && fy == ty) : ddx * ddx + ddy * ddy == 1;
+        gtd_end = !nav && (is_tog || act == 6);
+        success = success || (act == 6 && hit);
         coll = gtd_end && !success;  // counted as n_failure, reward 0
       }
       // ---- a5: reward and termination (Eq. 1, Tables 6-7)

@@ -104,7 +104,8 @@ def test_parity_row_f2_wide_grids(env_id):
     run_parity(env_id, 555, 500, block=555, seed=12)
 
 
-@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "LavaGapS7-v0", "Dynamic-Obstacles-8x8-v0"])
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "LavaGapS7-v0", "Dynamic-Obstacles-8x8-v0",
+                                    "GoToDoor-8x8-v0", "GoToDoor-5x5-v0"])
 def test_parity_reward_mode_navix(env_id):
     run_parity(env_id, 512, 300, block=512, reward_mode=1, seed=9)
 

@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("env_id,mode", [("DoorKey-8x8-v0", 0), ("LavaGapS7-v0", 1),
-                                         ("Dynamic-Obstacles-8x8-v0", 0), ("KeyCorridorS3R3-v0", 1)])
+                                         ("Dynamic-Obstacles-8x8-v0", 0), ("KeyCorridorS3R3-v0", 1),
+                                         ("GoToDoor-6x6-v0", 1), ("GoToDoor-6x6-v0", 0)])
 def test_reward_costs_parity(env_id, mode):
     from paper_2407_19396_b200 import NavixEnv
     n, K = 700, 150

@@ -368,3 +368,18 @@ def test_fourrooms_truncates_at_100():
         assert tr.all() == (t == 99)
     _, r, te, tr = env.step(np.zeros(4, np.uint8))
     assert env.export()[:, 3 * 289 + 5].tolist() == [0, 0, 0, 0]  # auto-reset: step_count 0
+
+
+def test_gotodoor_navix_mode_on_door_done():
+    # Table 6/7 `on_door_done` (R#39): only done *in front of* the mission's
+    # door rewards (+1) and terminates; toggle and other dones continue
+    env, outs = _room([F, 6], 3, (2, 0), reward_mode=1)        # (2,1) facing the target door
+    assert outs[1][1:] == (1.0, 1, 0)
+    env, outs = _room([F, 1, 6], 3, (2, 0), reward_mode=1)     # adjacent but facing east
+    assert outs[2][1:] == (0.0, 0, 0)
+    env, outs = _room([F, 5, 6], 3, (2, 0), reward_mode=1)     # toggle opens it, no termination; done still counts
+    assert outs[1][1:] == (0.0, 0, 0)
+    assert outs[2][1:] == (1.0, 1, 0)
+    env, outs = _room([F, 6], 3, (0, 2), reward_mode=1)        # facing a door of another colour
+    assert outs[1][1:] == (0.0, 0, 0)
+    assert env.stats()[0] == 0
