@@ -294,7 +294,16 @@ static void gen_dynobs(Env& e, DrawStream& ds) {
   e.grid = Grid(W, H);
   e.grid.wall_rect(0, 0, W, H);
   e.grid.set(W - 2, H - 2, make_goal());
-  e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
+  if (e.spec.random_start) {
+    // [MG] DynamicObstaclesEnv(agent_start_pos=None): place_agent(), then the balls
+    e.agent_x = -1; e.agent_y = -1;
+    int ax, ay;
+    place_uniform(e, 0, 0, W, H, ds.next(), nullptr, &ax, &ay);
+    e.agent_x = ax; e.agent_y = ay;
+    e.agent_dir = (int)ds.next_bounded(4);
+  } else {
+    e.agent_x = 1; e.agent_y = 1; e.agent_dir = 0;
+  }
   e.obstacles.clear();
   for (int i = 0; i < e.spec.n_obstacles; ++i) {
     int bx, by;

@@ -237,7 +237,8 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     if (s.size < 5 || s.size > 16) return false;
     s.max_steps = 10 * s.size * s.size;  // [MG] DoorKeyEnv
     s.n_actions = 7;
-  } else if (square("Dynamic-Obstacles-", F_DYNOBS)) {
+  } else if (square("Dynamic-Obstacles-", F_DYNOBS) ||
+             (square("Dynamic-Obstacles-Random-", F_DYNOBS) && (s.random_start = true))) {
     if (s.size < 4 || s.size > 16) return false;
     s.max_steps = 4 * s.size * s.size;  // [MG] DynamicObstaclesEnv
     s.n_actions = 3;                    // Discrete(forward + 1) (R#7)

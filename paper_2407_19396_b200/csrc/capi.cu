@@ -104,10 +104,11 @@ int parse_id(const char* env_id, EnvConfig* c) {
   } else if (sq("DoorKey-%dx%d%c") || sq("DoorKey-Random-%dx%d%c")) {  // R#36
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     *c = EnvConfig{FAM_DOORKEY, a, a, 10 * a * a, 7, 0, 0, 0};
-  } else if (sq("Dynamic-Obstacles-%dx%d%c")) {
+  } else if (sq("Dynamic-Obstacles-%dx%d%c") || sq("Dynamic-Obstacles-Random-%dx%d%c")) {
     if (a != 5 && a != 6 && a != 8 && a != 16) return 1;
     const int nob = a == 5 ? 2 : a == 6 ? 3 : a == 8 ? 4 : 8;  // R#6
-    *c = EnvConfig{FAM_DYNOBS, a, a, 4 * a * a, 3, nob, 0, 0};
+    const int random_start = id.find("-Random-") != std::string::npos;  // R#40
+    *c = EnvConfig{FAM_DYNOBS, a, a, 4 * a * a, 3, nob, 0, 0, random_start};
   } else if (sscanf(id.c_str(), "LavaGapS%d%c", &a, &tail) == 1) {
     if (a < 5 || a > 7) return 1;
     *c = EnvConfig{FAM_LAVAGAP, a, a, 4 * a * a, 7, 0, 0, 0};

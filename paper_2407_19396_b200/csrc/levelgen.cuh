@@ -59,6 +59,8 @@ template <int RW>
 struct RowViewT {
   uint64_t* rows;  // &planes[0][tid]
   __device__ __forceinline__ uint8_t* at(int x, int y) const {
+    if constexpr (RW == 1)  // one plane per row: x is the byte within it (x < 8)
+      return reinterpret_cast<uint8_t*>(rows) + y * (TILE * 8) + x;
     return reinterpret_cast<uint8_t*>(rows + (y * RW + (x >> 3)) * TILE) + (x & 7);
   }
   __device__ __forceinline__ uint8_t get(int x, int y) const { return *at(x, y); }
@@ -272,7 +274,20 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
 #pragma unroll
       for (int x = 1; x <= W - 2; ++x) freem[(y * RSB + x) >> 6] |= 1ull << ((y * RSB + x) & 63);
     freem[((H - 2) * RSB + (W - 2)) >> 6] &= ~(1ull << (((H - 2) * RSB + (W - 2)) & 63));  // goal
-    freem[(1 * RSB + 1) >> 6] &= ~(1ull << ((1 * RSB + 1) & 63));                           // agent (1, 1)
+    if (gparam) {
+      // Dynamic-Obstacles-Random: place_agent() over the empty cells (the goal
+      // is the last interior cell in row-major order), then a direction
+      const uint32_t k = ds.next_bounded((uint32_t)((W - 2) * (H - 2) - 1));
+      o.ax = 1 + (int)(k % (W - 2));
+      o.ay = 1 + (int)(k / (W - 2));
+      o.dir = (int)ds.next_bounded(4);
+    }
+    {
+      const int ab = o.ay * RSB + o.ax;  // the agent's cell
+#pragma unroll
+      for (int w = 0; w < NWD; ++w)
+        if (w == (ab >> 6)) freem[w] &= ~(1ull << (ab & 63));
+    }
 #pragma unroll
     for (int b = 0; b < C::NOBST; ++b) {
       const uint32_t u = ds.next();

@@ -223,11 +223,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
            st_fail = 0;
 
   const bool regen = MODE == MODE_RESET || (MODE == MODE_STEP && prev_done);
-  // Dynamic-Obstacles auto-resets ~10 % of its envs per step: left in place,
-  // nearly every warp would run the level generator for a few lanes.  Its
-  // resetting envs are queued per CTA instead and generated by the first
-  // threads (one warp for up to 32 of them), each into its env's SMEM rows.
-  constexpr bool COMPACT = FAM == FAM_DYNOBS && MODE == MODE_STEP;
+  // Dynamic-Obstacles auto-resets ~10 % of its envs per step (GoToDoor ~30 %
+  // under a random policy): left in place, nearly every warp would run the
+  // level generator for a few lanes.  Their resetting envs are queued per CTA
+  // instead and generated by the first threads (one warp for up to 32 of
+  // them), each into its env's SMEM rows.
+  constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   if (COMPACT) {
     __shared__ int s_qn;
     __shared__ int s_q[TILE];
@@ -248,14 +249,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       const GenOut o =
           generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi,
                                     a.gen_param);
-      s_qballs[st] = o.balls;
+      s_qballs[st] = FAM == FAM_GOTODOOR ? (uint64_t)o.target : o.balls;
       s_qout[st] = (uint32_t)o.ax | ((uint32_t)o.ay << 8) | ((uint32_t)o.dir << 16) | (o.fail << 24);
     }
     __syncthreads();
     if (regen) {
       const uint32_t o = s_qout[tid];
       episode = s_qep[tid];
-      balls = s_qballs[tid];
+      if (FAM == FAM_GOTODOOR) target = (uint32_t)s_qballs[tid];
+      else balls = s_qballs[tid];
       ax = (int)(o & 0xFF); ay = (int)((o >> 8) & 0xFF); dir = (int)((o >> 16) & 3);
       st_fail = o >> 24;
       carry = CELL_EMPTY;

@@ -36,6 +36,7 @@ def test_header_symbols_are_exported():
     ("Navix-DoorKey-Random-5x5", 5, 5, 250, 7, 1),
     ("Navix-GoToDoor-8x8-v0", 8, 8, 256, 7, 8),
     ("Navix-FourRooms-v0", 17, 17, 100, 7, 9),
+    ("MiniGrid-Dynamic-Obstacles-Random-6x6-v0", 6, 6, 144, 3, 2),
 ])
 def test_spec_of_table9_ids(env_id, h, w, T, na, fam):
     from oracle import spec_of as oracle_spec

@@ -383,3 +383,24 @@ def test_gotodoor_navix_mode_on_door_done():
     env, outs = _room([F, 6], 3, (0, 2), reward_mode=1)        # facing a door of another colour
     assert outs[1][1:] == (0.0, 0, 0)
     assert env.stats()[0] == 0
+
+
+@pytest.mark.parametrize("S,nob", [(5, 2), (6, 3), (8, 4)])
+def test_dynobs_random_start(S, nob):
+    # [MG] DynamicObstaclesEnv(agent_start_pos=None) (R#40): agent uniform over
+    # the empty interior cells and directions, then the balls avoid it
+    env_id = f"Dynamic-Obstacles-Random-{S}x{S}"
+    s = spec_of(env_id)
+    assert (s.width, s.max_steps, s.n_actions, s.n_obstacles) == (S, 4 * S * S, 3, nob)
+    n = 20000
+    env = OracleEnv(env_id, n, seed=4)
+    env.reset()
+    full = env.observe_full()
+    ag = np.argwhere(full[:, :, :, 0] == 10)
+    assert np.array_equal(ag[:, 0], np.arange(n))
+    x, y = ag[:, 1], ag[:, 2]
+    k = (S - 2) * (S - 2) - 1
+    cnt = np.bincount((y - 1) * (S - 2) + (x - 1), minlength=k + 1)
+    assert cnt[k] == 0 and sps.chisquare(cnt[:k]).pvalue > 1e-4
+    assert sps.chisquare(np.bincount(full[np.arange(n), x, y, 2], minlength=4)).pvalue > 1e-4
+    assert np.all(np.count_nonzero(full[:, :, :, 0] == 6, axis=(1, 2)) == nob)

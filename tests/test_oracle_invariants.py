@@ -19,7 +19,7 @@ ENVS = ["Empty-5x5-v0", "Empty-8x8-v0", "DoorKey-8x8-v0", "Dynamic-Obstacles-8x8
         "KeyCorridorS3R3-v0", "LavaGapS7-v0", "DoorKey-5x5-v0", "KeyCorridorS3R1-v0",
         "DoorKey-16x16-v0", "Dynamic-Obstacles-16x16-v0", "KeyCorridorS4R3-v0", "KeyCorridorS6R3-v0",
         "Empty-Random-8x8-v0", "DistShift1-v0", "DistShift2-v0", "SimpleCrossingS11N5-v0", "GoToDoor-8x8-v0",
-        "FourRooms-v0"]
+        "FourRooms-v0", "Dynamic-Obstacles-Random-6x6"]
 
 
 @pytest.mark.parametrize("env_id", ENVS)

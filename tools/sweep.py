@@ -32,6 +32,13 @@ CONFIGS = [  # (env id, largest N) per BASELINE.json configs
     ("DoorKey-16x16-v0", 1 << 20),
     ("Dynamic-Obstacles-16x16-v0", 1 << 20),
     ("KeyCorridorS6R3-v0", 1 << 20),
+    ("Empty-Random-8x8", 1 << 20),
+    ("DistShift1-v0", 1 << 20),
+    ("SimpleCrossingS9N3-v0", 1 << 20),
+    ("SimpleCrossingS11N5-v0", 1 << 20),
+    ("GoToDoor-8x8-v0", 1 << 20),
+    ("FourRooms-v0", 1 << 20),
+    ("Dynamic-Obstacles-Random-6x6", 1 << 20),
 ]
 SIZES = [1, 8, 1 << 10, 1 << 11, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 21, 1 << 22, 1 << 23]
 
