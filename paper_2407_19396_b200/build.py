@@ -1,15 +1,20 @@
 """Build libnavix.so in-tree with nvcc for sm_100a (no JIT cache, no CPU path)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libnavix.so")
-SOURCES = ["step_kernel.cu", "capi.cu"]
-HEADERS = ["layout.h", "philox.cuh", "levelgen.cuh", "obs.cuh", os.path.join("..", "..", "include", "navix.h")]
+# every translation unit: the C ABI, the dispatcher and one file of kernel
+# instantiations per family group (compiled in parallel)
+SOURCES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(CSRC, "*.cu")))
+HEADERS = ["layout.h", "philox.cuh", "levelgen.cuh", "obs.cuh", "step_kernel.cuh",
+           os.path.join("..", "..", "include", "navix.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -31,18 +36,24 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
-    objs = []
-    for src in SOURCES:
+    os.makedirs(os.path.join(HERE, "..", "build"), exist_ok=True)
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        with open(os.path.join(HERE, "..", "build", src.replace(".cu", ".ptxas.txt")), "w") as f:
+            f.write(r.stderr)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for src, obj, r in results:
         if verbose or r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-        os.makedirs(os.path.join(HERE, "..", "build"), exist_ok=True)
-        with open(os.path.join(HERE, "..", "build", src.replace(".cu", ".ptxas.txt")), "w") as f:
-            f.write(r.stderr)
         objs.append(obj)
     # default static cudart: the .so carries its own runtime, shares the
     # primary context (and stream handles) with torch's.

@@ -97,7 +97,7 @@ inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   return L;
 }
 
-// Tile-local env le <-> state slot (see step_kernel.cu): warp w lane l owns
+// Tile-local env le <-> state slot (see step_kernel.cuh): warp w lane l owns
 // env 4*l + w and slot 32*w + l.
 __host__ __device__ constexpr int slot_of_env(int le) { return (le & 3) * 32 + (le >> 2); }
 __host__ __device__ constexpr int env_of_slot(int slot) { return 4 * (slot & 31) + (slot >> 5); }

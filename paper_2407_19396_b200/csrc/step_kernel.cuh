@@ -1,4 +1,5 @@
-// step_kernel.cu — the fused batched MiniGrid step for sm_100a.
+// step_kernel.cuh — the fused batched MiniGrid step for sm_100a (kernel templates;
+// instantiated per family group in inst_*.cu, dispatched in dispatch.cu).
 //
 // One thread owns one environment; one CTA owns a tile of TILE = 128 envs.
 // Per env and step:
@@ -21,6 +22,7 @@
 //                 copy) per tile; reward/flags/agent records coalesced;
 //                 grid rows written back only when modified; episode
 //                 statistics warp-reduced into striped int64 counters.
+#pragma once
 #include <cstdint>
 #include <cstdlib>
 
@@ -93,7 +95,7 @@ __device__ __forceinline__ void transpose_lines(uint64_t* lines) {
     lines[x * TILE] = x < 4 ? ((uint64_t)b[x] << 32) | a[x] : ((uint64_t)d[x - 4] << 32) | c[x - 4];
 }
 
-__device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) {
+static __device__ __noinline__ float success_reward(int mode, uint32_t sc, uint32_t T) {
   if (mode == 1) return 1.0f;
   // R#2: binary64, [MG] order, no contraction, one rounding to binary32
   const double q = __ddiv_rn((double)sc, (double)T);
@@ -744,39 +746,14 @@ __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint
   }
 }
 
-// ------------------------------------------------------------------ other kernels
-__global__ void sample_actions_kernel(uint8_t* out, int64_t n, int64_t steps, uint32_t env_begin, uint32_t t0,
-                                      uint32_t klo, uint32_t khi, uint32_t n_actions) {
-  const int64_t total = n * steps;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / n, env = i % n;
-    const uint4 w = philox4x32_10(make_uint4(env_begin + (uint32_t)env, t0 + (uint32_t)t, 2u << 16, 0u), klo, khi);
-    out[i] = (uint8_t)bounded(w.x, n_actions);
-  }
-}
-
-__global__ void stats_reduce_kernel(const unsigned long long* slots, long long* out8) {
-  __shared__ unsigned long long part[8][32];
-  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;  // 256 threads: 8 counters x 32 lanes
-  unsigned long long s = 0;
-  for (int i = lane; i < NSLOT; i += 32) s += slots[(size_t)i * 8 + k];
-  part[k][lane] = s;
-  __syncthreads();
-  if (lane == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < 32; ++i) t += part[k][i];
-    out8[k] = (long long)t;
-  }
-}
-
 // ------------------------------------------------------------------ dispatch
 template <class K>
-static void allow_dyn_smem(K kernel, size_t bytes) {
+inline void allow_dyn_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int FAM, int H, int W>
-static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
+cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
   const dim3 block(TILE);
   using C = Cfg<FAM, H, W>;
   constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL>);
@@ -819,63 +796,6 @@ static cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cu
   } else {
     navix_kernel<FAM, H, W, MODE_OBSERVE><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   }
-  return cudaPeekAtLastError();
-}
-
-cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
-  const int key = c.family * 10000 + c.height * 100 + c.width;
-  switch (key) {
-    case FAM_EMPTY * 10000 + 505: return launch_fhw<FAM_EMPTY, 5, 5>(mode, a, n_tiles, s);
-    case FAM_EMPTY * 10000 + 606: return launch_fhw<FAM_EMPTY, 6, 6>(mode, a, n_tiles, s);
-    case FAM_EMPTY * 10000 + 808: return launch_fhw<FAM_EMPTY, 8, 8>(mode, a, n_tiles, s);
-    case FAM_DOORKEY * 10000 + 505: return launch_fhw<FAM_DOORKEY, 5, 5>(mode, a, n_tiles, s);
-    case FAM_DOORKEY * 10000 + 606: return launch_fhw<FAM_DOORKEY, 6, 6>(mode, a, n_tiles, s);
-    case FAM_DOORKEY * 10000 + 808: return launch_fhw<FAM_DOORKEY, 8, 8>(mode, a, n_tiles, s);
-    case FAM_DYNOBS * 10000 + 505: return launch_fhw<FAM_DYNOBS, 5, 5>(mode, a, n_tiles, s);
-    case FAM_DYNOBS * 10000 + 606: return launch_fhw<FAM_DYNOBS, 6, 6>(mode, a, n_tiles, s);
-    case FAM_DYNOBS * 10000 + 808: return launch_fhw<FAM_DYNOBS, 8, 8>(mode, a, n_tiles, s);
-    case FAM_LAVAGAP * 10000 + 505: return launch_fhw<FAM_LAVAGAP, 5, 5>(mode, a, n_tiles, s);
-    case FAM_LAVAGAP * 10000 + 606: return launch_fhw<FAM_LAVAGAP, 6, 6>(mode, a, n_tiles, s);
-    case FAM_LAVAGAP * 10000 + 707: return launch_fhw<FAM_LAVAGAP, 7, 7>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 307: return launch_fhw<FAM_KEYCORRIDOR, 3, 7>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 507: return launch_fhw<FAM_KEYCORRIDOR, 5, 7>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 707: return launch_fhw<FAM_KEYCORRIDOR, 7, 7>(mode, a, n_tiles, s);
-    // row f2: grids up to 16x16
-    case FAM_EMPTY * 10000 + 1616: return launch_fhw<FAM_EMPTY, 16, 16>(mode, a, n_tiles, s);
-    case FAM_DOORKEY * 10000 + 1616: return launch_fhw<FAM_DOORKEY, 16, 16>(mode, a, n_tiles, s);
-    case FAM_DYNOBS * 10000 + 1616: return launch_fhw<FAM_DYNOBS, 16, 16>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 1010: return launch_fhw<FAM_KEYCORRIDOR, 10, 10>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 1313: return launch_fhw<FAM_KEYCORRIDOR, 13, 13>(mode, a, n_tiles, s);
-    case FAM_KEYCORRIDOR * 10000 + 1616: return launch_fhw<FAM_KEYCORRIDOR, 16, 16>(mode, a, n_tiles, s);
-    case FAM_EMPTY_RANDOM * 10000 + 505: return launch_fhw<FAM_EMPTY_RANDOM, 5, 5>(mode, a, n_tiles, s);
-    case FAM_EMPTY_RANDOM * 10000 + 606: return launch_fhw<FAM_EMPTY_RANDOM, 6, 6>(mode, a, n_tiles, s);
-    case FAM_EMPTY_RANDOM * 10000 + 808: return launch_fhw<FAM_EMPTY_RANDOM, 8, 8>(mode, a, n_tiles, s);
-    case FAM_EMPTY_RANDOM * 10000 + 1616: return launch_fhw<FAM_EMPTY_RANDOM, 16, 16>(mode, a, n_tiles, s);
-    case FAM_DISTSHIFT1 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT1, 7, 9>(mode, a, n_tiles, s);
-    case FAM_DISTSHIFT2 * 10000 + 709: return launch_fhw<FAM_DISTSHIFT2, 7, 9>(mode, a, n_tiles, s);
-    case FAM_FOURROOMS * 10000 + 1717: return launch_fhw<FAM_FOURROOMS, 17, 17>(mode, a, n_tiles, s);
-    case FAM_GOTODOOR * 10000 + 505: return launch_fhw<FAM_GOTODOOR, 5, 5>(mode, a, n_tiles, s);
-    case FAM_GOTODOOR * 10000 + 606: return launch_fhw<FAM_GOTODOOR, 6, 6>(mode, a, n_tiles, s);
-    case FAM_GOTODOOR * 10000 + 808: return launch_fhw<FAM_GOTODOOR, 8, 8>(mode, a, n_tiles, s);
-    case FAM_CROSSING * 10000 + 909: return launch_fhw<FAM_CROSSING, 9, 9>(mode, a, n_tiles, s);
-    case FAM_CROSSING * 10000 + 1111: return launch_fhw<FAM_CROSSING, 11, 11>(mode, a, n_tiles, s);
-    default: return cudaErrorInvalidConfiguration;
-  }
-}
-
-cudaError_t launch_sample_actions(uint8_t* out, int64_t n, int64_t steps, uint32_t env_begin, uint32_t t0,
-                                  uint64_t seed, uint32_t n_actions, cudaStream_t s) {
-  const int64_t total = n * steps;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  if (blocks < 1) blocks = 1;
-  sample_actions_kernel<<<(unsigned)blocks, 256, 0, s>>>(out, n, steps, env_begin, t0, (uint32_t)seed,
-                                                         (uint32_t)(seed >> 32), n_actions);
-  return cudaPeekAtLastError();
-}
-
-cudaError_t launch_stats_reduce(const unsigned long long* slots, long long* out8, cudaStream_t s) {
-  stats_reduce_kernel<<<1, 256, 0, s>>>(slots, out8);
   return cudaPeekAtLastError();
 }
 

@@ -71,10 +71,13 @@ def main():
     lines = []
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(a.so)], cwd=d, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.startswith("step_kernel")]
-        if cub:
-            dis = run(["nvdisasm", "-g", "-c", os.path.join(d, cub[0])]).split("\n")
+        dis, st = [], []
+        for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):  # the TU holding the kernel
+            dis = run(["nvdisasm", "-g", "-c", os.path.join(d, cub)]).split("\n")
             st = [i for i, l in enumerate(dis) if l.startswith('//----') and a.kernel in l]
+            if st:
+                break
+        if st:
             if st:
                 en = [i for i, l in enumerate(dis[st[0] + 1:], st[0] + 1) if l.startswith('//----')]
                 seq, cur = [], None
