@@ -56,7 +56,7 @@ def committed_traffic(env_id: str):
 class ClockSampler:
     """NVML clocks + throttle reasons sampled in a thread during the timed region."""
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.samples, self.reasons = [], set()
         self.period, self.ok = period_s, False
         try:
@@ -259,18 +259,19 @@ def run_navix(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local_rank)
     barrier()
-    ev0.record(s)
-    if graphs:
-        for gph in graphs:
-            gph.replay()
-    else:
-        for t in range(args.steps):
-            env.step(acts[t % ring])
-    ev1.record(s)
-    # the launches are queued: sample clocks / throttle reasons from the host
-    # while the device is still inside the timed region
-    clk.poll_until(ev1)
-    torch.cuda.synchronize(dev)
+    with clk:  # background sampler thread (every 5 ms) for the whole timed region
+        ev0.record(s)
+        if graphs:
+            for gph in graphs:
+                gph.replay()
+        else:
+            for t in range(args.steps):
+                env.step(acts[t % ring])
+        ev1.record(s)
+        # the launches are queued: also sample clocks / throttle reasons from
+        # this thread while the device is still inside the timed region
+        clk.poll_until(ev1)
+        torch.cuda.synchronize(dev)
     t_local = ev0.elapsed_time(ev1) / 1e3
     t_max = max_over_ranks(t_local, dev)
     value = n_total * args.steps / t_max
@@ -304,6 +305,35 @@ def run_navix(args, rank, world, local_rank):
                    "frac_of_measured_hbm": Br * n * Kr / t_r / 1e9 / measured_peaks()[0],
                    "api": "navix_rollout (state on chip across the K steps; row f1)"}
         del outs
+
+    # f3: the same step emitting Table 5 `categorical_first_person` (49 B records)
+    categorical = None
+    if args.categorical_steps > 0:
+        Kc = min(args.categorical_steps, ring)
+        cenv = NavixEnv(args.env, n, seed=0, env_begin=begin, num_envs_total=n_total, device=dev,
+                        observation="categorical")
+        cenv.reset()
+        for t in range(args.warmup):
+            cenv.step(acts[t % ring])
+        torch.cuda.synchronize(dev)
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            for t in range(Kc):
+                cenv.step(acts[t])
+        gph.replay()
+        barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(s)
+        gph.replay()
+        c1.record(s)
+        torch.cuda.synchronize(dev)
+        t_c = max_over_ranks(c0.elapsed_time(c1) / 1e3 / Kc, dev)
+        Bc = B - 147 + 49
+        categorical = {"steps": Kc, "value": n_total / t_c, "unit": UNIT, "ms_per_step": 1e3 * t_c,
+                       "algorithmic_bytes_per_env_step": Bc, "achieved_GBps_per_gpu": Bc * n / t_c / 1e9,
+                       "frac_of_measured_hbm": Bc * n / t_c / 1e9 / measured_peaks()[0],
+                       "api": "navix_step with navix_set_observation(CATEGORICAL) (row f3)"}
+        del gph, cenv
 
     # end to end through the host-buffer C-ABI call (H2D actions, D2H outputs)
     h_act = torch.from_numpy(np.ascontiguousarray(acts[: args.e2e_steps].cpu().numpy())).pin_memory()
@@ -353,6 +383,7 @@ def run_navix(args, rank, world, local_rank):
                 "api": "navix_step_host (pinned host buffers)"},
         "gpu_launches": args.steps,
         "rollout": rollout,
+        "categorical": categorical,
         "clocks": clk.summary(),
         "episode_stats": {k: int(v) for k, v in zip(
             ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_failure", "n_truncated",
@@ -377,6 +408,7 @@ def main():
     ap.add_argument("--action-ring", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--rollout-steps", type=int, default=64)
+    ap.add_argument("--categorical-steps", type=int, default=200)
     ap.add_argument("--cpu-envs", type=int, default=4096)
     ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)

@@ -149,9 +149,20 @@ NAVIX_API navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64
  * Host only, takes effect for subsequently enqueued steps. */
 NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost);
 
+/* Observation kinds (Table 5; R#41).  SYMBOLIC (the
+ * default): first-person records uint8[7][7][3] = 147 B (symbolic_first_person)
+ * and full grids uint8[W][H][3] (symbolic).  CATEGORICAL: the entity type
+ * alone, uint8[7][7] = 49 B (categorical_first_person) and uint8[W][H]
+ * (categorical); unseen view cells are 0.  The kind applies to every obs
+ * output enqueued afterwards (reset, step, step_host, rollout, observe,
+ * observe_full); size obs buffers accordingly.  Host only. */
+enum { NAVIX_OBS_SYMBOLIC = 0, NAVIX_OBS_CATEGORICAL = 1 };
+NAVIX_API navix_status navix_set_observation(navix_env* h, int kind);
+
 /* Table 5 `symbolic` full-grid observation, MiniGrid's
  * FullyObsWrapper: out (dev) uint8[n][width][height][3] ([x][y][c]), every
- * cell encoded (type, colour, state) and the agent cell (10, 0, dir) (R#32). */
+ * cell encoded (type, colour, state) and the agent cell (10, 0, dir) (R#32);
+ * uint8[n][width][height] (types, agent 10) with NAVIX_OBS_CATEGORICAL. */
 NAVIX_API navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream);
 
 /* The current observation of every env without stepping (O: S -> O, Table 3). */

@@ -31,6 +31,7 @@ struct navix_env {
   uint64_t seed;
   int device;
   int reward_mode;
+  int obs_kind = 0;  // ObsKind (navix_set_observation)
   float time_cost = 0.f, action_cost = 0.f;
   uint8_t* state;
   bool owns_state;
@@ -152,6 +153,7 @@ KernelArgs make_args(navix_env* h) {
   a.time_cost = h->time_cost;
   a.action_cost = h->action_cost;
   a.gen_param = h->cfg.gen_param;
+  a.obs_kind = h->obs_kind;
   return a;
 }
 
@@ -333,6 +335,14 @@ navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_
   return NAVIX_OK;
 }
 
+navix_status navix_set_observation(navix_env* h, int kind) {
+  if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_observation: null handle");
+  if (kind != NAVIX_OBS_SYMBOLIC && kind != NAVIX_OBS_CATEGORICAL)
+    return fail(NAVIX_E_INVALID_ARG, "unknown observation kind %d", kind);
+  h->obs_kind = kind;
+  return NAVIX_OK;
+}
+
 navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream) {
   if (!h || !out) return fail(NAVIX_E_INVALID_ARG, "navix_observe_full: null argument");
   KernelArgs a = make_args(h);
@@ -382,7 +392,8 @@ navix_status navix_step_host(navix_env* h, const uint8_t* actions, uint8_t* obs,
     return cuda_fail(e, "H2D actions");
   navix_status st = navix_step(h, h->h_actions, h->h_obs, h->h_reward, h->h_term, h->h_trunc, stream);
   if (st != NAVIX_OK) return st;
-  if ((e = cudaMemcpyAsync(obs, h->h_obs, n * OBS_BYTES, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+  if ((e = cudaMemcpyAsync(obs, h->h_obs, n * obs_record_bytes(h->obs_kind), cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
       (e = cudaMemcpyAsync(reward, h->h_reward, n * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
       (e = cudaMemcpyAsync(terminated, h->h_term, n, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
       (e = cudaMemcpyAsync(truncated, h->h_trunc, n, cudaMemcpyDeviceToHost, s)) != cudaSuccess)

@@ -33,6 +33,11 @@ namespace navix {
 constexpr int TILE = 128;   // envs per CTA (one thread per env)
 constexpr int NSLOT = 512;  // stats stripes (atomics spread over 512 x 64 B)
 constexpr int OBS_BYTES = 147;
+// Observation kinds (Table 5, R#41): the first-person record is
+// 147 B (symbolic, [vi][vj][type, colour, state]) or 49 B (categorical,
+// [vi][vj] entity type); the full grid is 3*W*H or W*H bytes, [x][y](c).
+enum ObsKind : int { OBS_SYMBOLIC = 0, OBS_CATEGORICAL = 1 };
+__host__ __device__ constexpr int obs_record_bytes(int kind) { return kind == OBS_CATEGORICAL ? 49 : OBS_BYTES; }
 
 enum Kind : uint8_t {
   K_OOB = 0, K_EMPTY = 1, K_WALL = 2, K_FLOOR = 3, K_DOOR_OPEN = 4, K_KEY = 5, K_BALL = 6,
@@ -124,6 +129,7 @@ struct KernelArgs {
   int bulk_act;         // 1: actions base is 16-B aligned -> cp.async.bulk load of full tiles
   int64_t rollout_steps;  // K of navix_rollout
   int gen_param;        // EnvConfig::gen_param (runtime level-generator parameter)
+  int obs_kind;         // ObsKind of the obs outputs
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };

@@ -325,13 +325,10 @@ __device__ __forceinline__ void view_oob_walls(int ax, int ay, int dir, uint32_t
   }
 }
 
-// Everything after the view columns: opacity, process_vis, encode, emission.
-// out: word-aligned SMEM address at or before this env's record, whose first
-// byte is at misalignment M (warp-uniform, 0..3).  All 7 columns are encoded
-// first; only the emission is specialised on M (one warp-uniform switch), so
-// the four variants share the rest of the code.
-__device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)[7], uint32_t carry, uint32_t* out,
-                                             int M) {
+// process_vis of the 7x7 view (byte vj of vis_lo / vis_hi has bit vi set iff
+// view cell (vi, vj) is visible).
+__device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const uint32_t (&chi)[7], uint32_t& vis_lo,
+                                                uint32_t& vis_hi) {
   // opacity rows: byte vj of op has bit vi set iff cell (vi, vj) is opaque
   uint32_t op_lo = 0, op_hi = 0;
 #pragma unroll
@@ -346,7 +343,8 @@ __device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)
   // rows vj = 6 .. 0 ([MG] process_vis order): V = R(S) | L(S), computed as
   // one carry chain on X = S | rev(S) << 8 over T2 = T | rev(T) << 8 (bit 7 = 0
   // stops the carry between the halves)
-  uint32_t vis_lo = 0, vis_hi = 0;
+  vis_lo = 0;
+  vis_hi = 0;
   uint32_t seed = 1u << 3;  // bits 0-6 (bit 7 may hold garbage: the carry stopper absorbs it)
 #pragma unroll
   for (int j = 6; j >= 0; --j) {
@@ -363,6 +361,17 @@ __device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)
     if (j < 4) vis_lo |= v << (8 * j);
     else vis_hi |= v << (8 * (j - 4));
   }
+}
+
+// Everything after the view columns: opacity, process_vis, encode, emission.
+// out: word-aligned SMEM address at or before this env's record, whose first
+// byte is at misalignment M (warp-uniform, 0..3).  All 7 columns are encoded
+// first; only the emission is specialised on M (one warp-uniform switch), so
+// the four variants share the rest of the code.
+__device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)[7], uint32_t carry, uint32_t* out,
+                                             int M) {
+  uint32_t vis_lo, vis_hi;
+  view_visibility(clo, chi, vis_lo, vis_hi);
   // the agent sees what it carries (R#13): view cell (3, 6), always visible
   chi[3] = prmt(chi[3], carry, 0x3410u);
   uint32_t r[7][7];
@@ -377,6 +386,82 @@ __device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)
     case 1: emit_record<1>(out, r); break;
     case 2: emit_record<2>(out, r); break;
     default: emit_record<3>(out, r); break;
+  }
+}
+
+// ---------------------------------------------------------------- categorical
+// categorical_first_person (Table 5, R#41): the 49-byte record of view
+// cell types [vi][vj].  Stream byte i of the record is type byte i % 7 of
+// column i / 7; word K of the word-aligned output gathers its <= 4 bytes from
+// at most two type registers (t[2 vi] = vj 0..3, t[2 vi + 1] = vj 4..6), so
+// one byte permute per word with a compile-time selector.
+struct CatPlan {
+  int p0, p1;      // valid byte range of the word (p0 > p1: nothing to store)
+  int s0, s1;      // source registers
+  uint32_t sel;
+};
+__host__ __device__ constexpr CatPlan cat_plan(int M, int K) {
+  CatPlan P{4, -1, 0, 0, 0u};
+  int src[2] = {-1, -1};
+  uint32_t sel = 0;
+  for (int p = 0; p < 4; ++p) {
+    const int i = 4 * K + p - M;
+    if (i < 0 || i > 48) continue;
+    if (P.p0 > p) P.p0 = p;
+    P.p1 = p;
+    const int col = i / 7, vj = i % 7;
+    const int reg = 2 * col + (vj >= 4 ? 1 : 0), byt = vj & 3;
+    int slot = src[0] == reg ? 0 : src[1] == reg ? 1 : src[0] < 0 ? 0 : 1;
+    src[slot] = reg;
+    sel |= (uint32_t)(4 * slot + byt) << (4 * p);
+  }
+  P.s0 = src[0] < 0 ? 0 : src[0];
+  P.s1 = src[1] < 0 ? P.s0 : src[1];
+  P.sel = sel;
+  return P;
+}
+template <int M, int K>
+__device__ __forceinline__ void emit_cat_word(uint32_t* out, const uint32_t (&t)[14]) {
+  constexpr CatPlan P = cat_plan(M, K);
+  if constexpr (P.p0 <= P.p1) {
+    const uint32_t v = prmt(t[P.s0], t[P.s1], P.sel);
+    if constexpr (P.p0 == 0 && P.p1 == 3) out[K] = v;
+    else sts_bytes(out + K, v, P.p0, P.p1);
+  }
+}
+template <int M>
+__device__ __forceinline__ void emit_cat_record(uint32_t* out, const uint32_t (&t)[14]) {
+  emit_cat_word<M, 0>(out, t);  emit_cat_word<M, 1>(out, t);  emit_cat_word<M, 2>(out, t);
+  emit_cat_word<M, 3>(out, t);  emit_cat_word<M, 4>(out, t);  emit_cat_word<M, 5>(out, t);
+  emit_cat_word<M, 6>(out, t);  emit_cat_word<M, 7>(out, t);  emit_cat_word<M, 8>(out, t);
+  emit_cat_word<M, 9>(out, t);  emit_cat_word<M, 10>(out, t); emit_cat_word<M, 11>(out, t);
+  emit_cat_word<M, 12>(out, t);
+}
+// type-only SWAR encode (encode4 without colour and state)
+__device__ __forceinline__ uint32_t encode4_type(uint32_t w, uint32_t m) {
+  const uint32_t E = w & m & 0x0F0F0F0Fu;
+  uint32_t D;
+  asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(D) : "r"(E + 0x75757575u));
+  return (E & ~D) | (D & 0x04040404u);
+}
+__device__ __forceinline__ void observe_cols_cat(uint32_t (&clo)[7], uint32_t (&chi)[7], uint32_t carry,
+                                                 uint32_t* out, int M) {
+  uint32_t vis_lo, vis_hi;
+  view_visibility(clo, chi, vis_lo, vis_hi);
+  chi[3] = prmt(chi[3], carry, 0x3410u);  // the agent sees what it carries (R#13)
+  uint32_t t[14];
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    const uint32_t m_lo = prmt(vis_lo * (1u << (7 - vi)), 0u, 0xBA98u);
+    const uint32_t m_hi = prmt(vis_hi * (1u << (7 - vi)), 0u, 0xBA98u);
+    t[2 * vi] = encode4_type(clo[vi], m_lo);
+    t[2 * vi + 1] = encode4_type(chi[vi], m_hi);
+  }
+  switch (M) {
+    case 0: emit_cat_record<0>(out, t); break;
+    case 1: emit_cat_record<1>(out, t); break;
+    case 2: emit_cat_record<2>(out, t); break;
+    default: emit_cat_record<3>(out, t); break;
   }
 }
 

@@ -193,7 +193,7 @@ __device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile
 // row lines (stride TILE); scratch: 8 more lines for the column view of odd
 // directions, or nullptr to transpose the rows in place (then the rows are
 // written back to HBM first if the grid changed, and are lost).
-template <int FAM, int H, int W, int MODE, class BeforeEmit>
+template <int FAM, int H, int W, int MODE, int OBSK, class BeforeEmit>
 __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t tile, uint64_t* rows, uint64_t* scratch,
                                                   const EnvIn& in, uint8_t* s_obs, BeforeEmit before_emit) {
   using C = Cfg<FAM, H, W>;
@@ -448,13 +448,16 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   before_emit();
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
-    const int M = (3 * warp) & 3;  // warp-uniform record misalignment (147*le mod 4)
+    constexpr int OB = obs_record_bytes(OBSK);
+    // warp-uniform record misalignment: 147*le mod 4 = 3w mod 4, 49*le mod 4 = w
+    const int M = OBSK == OBS_CATEGORICAL ? warp & 3 : (3 * warp) & 3;
     uint32_t clo[7], chi[7];
     if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
     else if constexpr (RW == 2) view_columns_wide(rows, ax, ay, dir, clo, chi);
     else view_columns_big<RW, H>(rows, ax, ay, dir, clo, chi);
     if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
-    observe_cols(clo, chi, carry, s32 + ((le * OBS_BYTES - M) >> 2), M);
+    if constexpr (OBSK == OBS_CATEGORICAL) observe_cols_cat(clo, chi, carry, s32 + ((le * OB - M) >> 2), M);
+    else observe_cols(clo, chi, carry, s32 + ((le * OB - M) >> 2), M);
   }
 
   EnvResult r;
@@ -476,21 +479,23 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 
 // a7: the tile's obs leave SMEM in one TMA bulk store (full tile, 16-B aligned
 // destination) issued by one thread, else with plain stores by `nthr` threads.
+template <int OBSK>
 __device__ __forceinline__ void store_obs(const KernelArgs& a, int64_t tile, const uint8_t* s_obs, int t, int nthr,
                                           bool issuer) {
+  constexpr int OB = obs_record_bytes(OBSK);
   const int64_t tile0 = tile * TILE;
   const int64_t nv = a.n - tile0;
   const int nvalid = nv >= TILE ? TILE : (int)nv;
-  uint8_t* dst = a.obs + tile0 * OBS_BYTES;
+  uint8_t* dst = a.obs + tile0 * OB;
   if (a.bulk_obs && nvalid == TILE) {
     if (issuer) {
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(s_obs)),
-                   "r"((uint32_t)(TILE * OBS_BYTES))
+                   "r"((uint32_t)(TILE * OB))
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   } else {
-    for (int i = t; i < nvalid * OBS_BYTES; i += nthr) dst[i] = s_obs[i];
+    for (int i = t; i < nvalid * OB; i += nthr) dst[i] = s_obs[i];
   }
 }
 
@@ -531,19 +536,19 @@ __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, co
 // ------------------------------------------------------------------ kernels
 // One tile per CTA (reset, observe; step when NAVIX_STEP_KERNEL=onetile).
 // 28 KB of SMEM: up to 8 CTAs per SM with <= 64 registers.
-template <int FAM, int NPL>
+template <int FAM, int NPL, int OBSK>
 struct OneTileSmem {
-  uint8_t obs[TILE * OBS_BYTES];
+  uint8_t obs[TILE * obs_record_bytes(OBSK)];
   TileSmem<FAM, NPL> buf;
   uint64_t scratch[NPL == 8 ? 8 : 1][TILE];  // rollout: column view of odd directions (narrow grids)
   uint64_t mbar;
 };
 extern __shared__ __align__(128) uint8_t navix_dyn_smem[];
 
-template <int FAM, int H, int W, int MODE>
+template <int FAM, int H, int W, int MODE, int OBSK>
 __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const KernelArgs a) {
   using C = Cfg<FAM, H, W>;
-  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL>*>(navix_dyn_smem);
+  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
   if (MODE != MODE_RESET) {
     const uint32_t mbar = smem_u32(&S.mbar);
     if (threadIdx.x == 0) {
@@ -553,11 +558,11 @@ __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const Kern
     __syncthreads();  // mbarrier initialised before anyone waits on it
     mbar_wait(mbar, 0);
   }
-  const EnvResult r = tile_compute<FAM, H, W, MODE>(a, blockIdx.x, &S.buf.rows[0][threadIdx.x], nullptr,
+  const EnvResult r = tile_compute<FAM, H, W, MODE, OBSK>(a, blockIdx.x, &S.buf.rows[0][threadIdx.x], nullptr,
                                                     decode_staged<FAM, MODE>(a, blockIdx.x, S.buf), S.obs, [] {});
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  store_obs(a, blockIdx.x, S.obs, threadIdx.x, TILE, threadIdx.x == 0);
+  store_obs<OBSK>(a, blockIdx.x, S.obs, threadIdx.x, TILE, threadIdx.x == 0);
   tile_store<FAM, MODE>(a, blockIdx.x, r);
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -572,9 +577,9 @@ __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const Kern
 // variant where the last warp to finish issues the store measured 1.3 % slower:
 // its warps spin on mbarriers instead.)  The last CTA to finish resets the
 // scheduler, so the kernel replays from a CUDA graph.
-template <int FAM, int H, int W>
+template <int FAM, int H, int W, int OBSK>
 __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
-  __shared__ __align__(128) uint8_t s_obs[TILE * OBS_BYTES];
+  __shared__ __align__(128) uint8_t s_obs[TILE * obs_record_bytes(OBSK)];
   using C = Cfg<FAM, H, W>;
   __shared__ __align__(128) TileSmem<FAM, C::NPL> s_buf[2];
   __shared__ __align__(8) uint64_t s_mbar[2];   // tile inputs landed (per buffer)
@@ -605,7 +610,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     // claim the tile-after-next now: the atomic's latency hides behind the compute
     unsigned int next = 0;
     if (tid == 0) next = atomicAdd(&sched[0], 1u);
-    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK>(
         a, tile, &s_buf[cur].rows[0][tid], nullptr, decode_staged<FAM, MODE_STEP>(a, tile, s_buf[cur]), s_obs, [&] {
       if (it > 0) {  // the previous tile's store must have read s_obs
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -614,7 +619,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     });
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // all records in s_obs; input buffer cur no longer read
-    store_obs(a, tile, s_obs, tid, TILE, tid == 0);
+    store_obs<OBSK>(a, tile, s_obs, tid, TILE, tid == 0);
     if (tid == 0) publish(cur, next);  // tile-after-next into the released buffer
     tile_store<FAM, MODE_STEP>(a, tile, r);
   }
@@ -633,10 +638,10 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
 // the K steps; per step only the actions come in and obs / reward / flags go
 // out (154 B per DoorKey env-step instead of 234).  Bit-identical to K
 // navix_step calls; outputs of step t at [t][n].
-template <int FAM, int H, int W>
+template <int FAM, int H, int W, int OBSK>
 __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a, int64_t K) {
   using C = Cfg<FAM, H, W>;
-  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL>*>(navix_dyn_smem);
+  auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
   uint8_t* const s_obs = S.obs;
   auto& s_buf = S.buf;
   auto& s_scratch = S.scratch;
@@ -658,12 +663,12 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     in.act = next_act;
     if (t + 1 < K && valid) next_act = a.actions[(t + 1) * a.n + e];  // one step ahead
     KernelArgs as = a;
-    as.obs = a.obs + t * a.n * OBS_BYTES;
+    as.obs = a.obs + t * a.n * obs_record_bytes(OBSK);
     as.reward = a.reward + t * a.n;
     as.terminated = a.terminated + t * a.n;
     as.truncated = a.truncated + t * a.n;
     as.bulk_obs = (reinterpret_cast<uintptr_t>(as.obs) & 15u) == 0;
-    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP>(as, tile, &s_buf.rows[0][tid],
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK>(as, tile, &s_buf.rows[0][tid],
                                                            C::RW == 1 ? &s_scratch[0][tid] : nullptr, in,
                                                            s_obs, [&] {
       if (t > 0) {  // the previous step's store must have read s_obs
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     });
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    store_obs(as, tile, s_obs, tid, TILE, tid == 0);
+    store_obs<OBSK>(as, tile, s_obs, tid, TILE, tid == 0);
     tile_store<FAM, MODE_STEP, false>(as, tile, r);
     in.rec = r.nrec;
     in.episode = r.episode;
@@ -698,9 +703,10 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
 // FullyObsWrapper — every cell (type, colour, state), the agent cell replaced
 // by (10 agent, 0 red, dir); memory order [x][y][c] (R#32).  Not on the step
 // path: one thread per env, staged in SMEM, coalesced copy-out.
-template <int FAM, int H, int W>
+template <int FAM, int H, int W, int OBSK>
 __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint8_t* out) {
-  constexpr int PER = 3 * W * H, RW = row_planes(W);
+  constexpr int CH = OBSK == OBS_CATEGORICAL ? 1 : 3;  // categorical: the entity type only (R#41)
+  constexpr int PER = CH * W * H, RW = row_planes(W);
   constexpr bool STAGE = TILE * PER <= 32 * 1024;  // small grids: SMEM staging + coalesced copy-out
   __shared__ __align__(16) uint8_t s_out[STAGE ? TILE * PER : 16];
   const int tid = threadIdx.x, le = 4 * (tid & 31) + (tid >> 5);
@@ -733,10 +739,12 @@ __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint
       const uint32_t c = (uint32_t)(pl[y * RW + (x >> 3)] >> (8 * (x & 7))) & 0xFF, kind = c & 15;
       const bool ag = x == ax && y == ay;
       if (write) {
-        uint8_t* t = o + (x * H + y) * 3;
+        uint8_t* t = o + (x * H + y) * CH;
         t[0] = ag ? 10 : (kind >= 11 ? 4 : kind);
-        t[1] = ag ? 0 : (c >> 4) & 7;
-        t[2] = ag ? dir : (kind >= 11 ? kind - 10 : 0);
+        if (CH == 3) {
+          t[1] = ag ? 0 : (c >> 4) & 7;
+          t[2] = ag ? dir : (kind >= 11 ? kind - 10 : 0);
+        }
       }
     }
   if (STAGE) {
@@ -752,17 +760,17 @@ inline void allow_dyn_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int FAM, int H, int W>
-cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
+template <int FAM, int H, int W, int OBSK>
+cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
   const dim3 block(TILE);
   using C = Cfg<FAM, H, W>;
-  constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL>);
+  constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL, OBSK>);
   static bool attrs = false;
   if (!attrs) {
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_STEP>, DYN);
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_RESET>, DYN);
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_OBSERVE>, DYN);
-    allow_dyn_smem(navix_rollout_kernel<FAM, H, W>, DYN);
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_STEP, OBSK>, DYN);
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_RESET, OBSK>, DYN);
+    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_OBSERVE, OBSK>, DYN);
+    allow_dyn_smem(navix_rollout_kernel<FAM, H, W, OBSK>, DYN);
     attrs = true;
   }
   static int onetile = -1;
@@ -771,7 +779,7 @@ cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStrea
     onetile = v && v[0] == 'o';
   }
   if (mode == MODE_STEP && (onetile || W > 8)) {  // wide grids: one tile per CTA (SMEM)
-    navix_kernel<FAM, H, W, MODE_STEP><<<(unsigned)n_tiles, block, DYN, s>>>(a);
+    navix_kernel<FAM, H, W, MODE_STEP, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   } else if (mode == MODE_STEP) {
     if constexpr (W <= 8) {
       // persistent grid: as many CTAs as fit on the device at once
@@ -780,23 +788,29 @@ cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStrea
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W>, TILE, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE, 0);
         if (per_sm < 1) per_sm = 1;
       }
       const int64_t cap = (int64_t)per_sm * n_sm;
       const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
-      navix_step_persistent<FAM, H, W><<<grid, block, 0, s>>>(a);
+      navix_step_persistent<FAM, H, W, OBSK><<<grid, block, 0, s>>>(a);
     }
   } else if (mode == MODE_FULL_OBS) {
-    full_obs_kernel<FAM, H, W><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
+    full_obs_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
   } else if (mode == MODE_ROLLOUT) {
-    navix_rollout_kernel<FAM, H, W><<<(unsigned)n_tiles, block, DYN, s>>>(a, a.rollout_steps);
+    navix_rollout_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a, a.rollout_steps);
   } else if (mode == MODE_RESET) {
-    navix_kernel<FAM, H, W, MODE_RESET><<<(unsigned)n_tiles, block, DYN, s>>>(a);
+    navix_kernel<FAM, H, W, MODE_RESET, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   } else {
-    navix_kernel<FAM, H, W, MODE_OBSERVE><<<(unsigned)n_tiles, block, DYN, s>>>(a);
+    navix_kernel<FAM, H, W, MODE_OBSERVE, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   }
   return cudaPeekAtLastError();
+}
+
+template <int FAM, int H, int W>
+cudaError_t launch_fhw(int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
+  return a.obs_kind == OBS_CATEGORICAL ? launch_fhwk<FAM, H, W, OBS_CATEGORICAL>(mode, a, n_tiles, s)
+                                       : launch_fhwk<FAM, H, W, OBS_SYMBOLIC>(mode, a, n_tiles, s);
 }
 
 }  // namespace navix

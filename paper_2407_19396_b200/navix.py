@@ -20,11 +20,14 @@ _lib = None
 
 NAVIX_OK, NAVIX_E_UNKNOWN_ENV, NAVIX_E_INVALID_ARG, NAVIX_E_CUDA, NAVIX_E_NOMEM, NAVIX_E_UNSUPPORTED = range(6)
 REWARD_MINIGRID, REWARD_NAVIX = 0, 1
+# observation kinds (Table 5; include/navix.h NAVIX_OBS_*)
+OBS_SYMBOLIC, OBS_CATEGORICAL = 0, 1
+_OBS_KINDS = {"symbolic": OBS_SYMBOLIC, "categorical": OBS_CATEGORICAL}
 STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
                 "n_lava", "n_failure", "n_truncated", "gen_failures")
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
-    "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -76,6 +79,7 @@ def load_library():
         "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
         "navix_observe_full": ([P, P, P], I32),
         "navix_set_reward_costs": ([P, ctypes.c_float, ctypes.c_float], I32),
+        "navix_set_observation": ([P, I32], I32),
         "navix_sample_actions": ([P, U64, I64, I64, P, P], I32),
         "navix_step_host": ([P, P, P, P, P, P, P], I32),
         "navix_stats": ([P, P, P], I32),
@@ -124,12 +128,15 @@ class NavixEnv:
     ``reset()`` / ``step(actions)`` return CUDA tensors written by the kernels:
     obs uint8[n, 7, 7, 3] ([vi][vj][channel]), reward float32[n],
     terminated / truncated bool-valued uint8[n].  Output tensors are reused
-    between calls unless ``out=`` is given.
+    between calls unless ``out=`` is given.  ``observation="categorical"``
+    (Table 5 categorical / categorical_first_person) makes every obs output
+    the entity type alone: uint8[n, 7, 7] and uint8[n, width, height].
     """
 
     def __init__(self, env_id: str, num_envs: int, seed: int = 0, *, device=None,
                  reward_mode: int = REWARD_MINIGRID, env_begin: int = 0,
-                 num_envs_total: int | None = None, state: torch.Tensor | None = None):
+                 num_envs_total: int | None = None, state: torch.Tensor | None = None,
+                 observation: str = "symbolic"):
         if not torch.cuda.is_available():
             raise RuntimeError("NavixEnv needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
@@ -147,8 +154,15 @@ class NavixEnv:
             env_id.encode(), self.n_total, self.env_begin, self.n, self.seed & (2 ** 64 - 1),
             self.device.index, None if state is None else _ptr(state), reward_mode, ctypes.byref(h)))
         self.h = h
+        if observation not in _OBS_KINDS:
+            raise ValueError(f"observation must be one of {sorted(_OBS_KINDS)}")
+        self.observation = observation
+        _check(self.lib.navix_set_observation(self.h, _OBS_KINDS[observation]))
+        self.obs_shape = (7, 7, 3) if observation == "symbolic" else (7, 7)
+        s = self.spec
+        self.full_shape = (s.width, s.height, 3) if observation == "symbolic" else (s.width, s.height)
         dev = self.device
-        self.obs = torch.empty((self.n, 7, 7, 3), dtype=torch.uint8, device=dev)
+        self.obs = torch.empty((self.n, *self.obs_shape), dtype=torch.uint8, device=dev)
         self.reward = torch.empty(self.n, dtype=torch.float32, device=dev)
         self.terminated = torch.empty(self.n, dtype=torch.uint8, device=dev)
         self.truncated = torch.empty(self.n, dtype=torch.uint8, device=dev)
@@ -168,7 +182,7 @@ class NavixEnv:
 
     def reset(self, out: torch.Tensor | None = None) -> torch.Tensor:
         obs = self.obs if out is None else out
-        self._check_out(obs, (self.n, 7, 7, 3), torch.uint8)
+        self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
         _check(self.lib.navix_reset(self.h, _ptr(obs), _stream(self.device)))
         return obs
 
@@ -176,7 +190,7 @@ class NavixEnv:
         self._check_out(actions, (self.n,), torch.uint8)
         obs, rew, term, trunc = out if out is not None else (
             self.obs, self.reward, self.terminated, self.truncated)
-        self._check_out(obs, (self.n, 7, 7, 3), torch.uint8)
+        self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
         self._check_out(rew, (self.n,), torch.float32)
         self._check_out(term, (self.n,), torch.uint8)
         self._check_out(trunc, (self.n,), torch.uint8)
@@ -193,12 +207,12 @@ class NavixEnv:
         self._check_out(actions, (K, self.n), torch.uint8)
         dev = self.device
         if out is None:
-            out = (torch.empty((K, self.n, 7, 7, 3), dtype=torch.uint8, device=dev),
+            out = (torch.empty((K, self.n, *self.obs_shape), dtype=torch.uint8, device=dev),
                    torch.empty((K, self.n), dtype=torch.float32, device=dev),
                    torch.empty((K, self.n), dtype=torch.uint8, device=dev),
                    torch.empty((K, self.n), dtype=torch.uint8, device=dev))
         obs, rew, term, trunc = out
-        self._check_out(obs, (K, self.n, 7, 7, 3), torch.uint8)
+        self._check_out(obs, (K, self.n, *self.obs_shape), torch.uint8)
         self._check_out(rew, (K, self.n), torch.float32)
         self._check_out(term, (K, self.n), torch.uint8)
         self._check_out(trunc, (K, self.n), torch.uint8)
@@ -211,16 +225,16 @@ class NavixEnv:
         _check(self.lib.navix_set_reward_costs(self.h, time_cost, action_cost))
 
     def observe_full(self, out: torch.Tensor | None = None) -> torch.Tensor:
-        """Table 5 `symbolic`: uint8[n, width, height, 3], agent cell (10, 0, dir)."""
-        s = self.spec
-        o = torch.empty((self.n, s.width, s.height, 3), dtype=torch.uint8, device=self.device) if out is None else out
-        self._check_out(o, (self.n, s.width, s.height, 3), torch.uint8)
+        """Table 5 `symbolic`: uint8[n, width, height, 3], agent cell (10, 0, dir)
+        (`categorical`: uint8[n, width, height], agent 10)."""
+        o = torch.empty((self.n, *self.full_shape), dtype=torch.uint8, device=self.device) if out is None else out
+        self._check_out(o, (self.n, *self.full_shape), torch.uint8)
         _check(self.lib.navix_observe_full(self.h, _ptr(o), _stream(self.device)))
         return o
 
     def observe(self, out: torch.Tensor | None = None) -> torch.Tensor:
         obs = self.obs if out is None else out
-        self._check_out(obs, (self.n, 7, 7, 3), torch.uint8)
+        self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
         _check(self.lib.navix_observe(self.h, _ptr(obs), _stream(self.device)))
         return obs
 
@@ -234,7 +248,7 @@ class NavixEnv:
     def step_host(self, actions: torch.Tensor, obs: torch.Tensor, reward: torch.Tensor,
                   terminated: torch.Tensor, truncated: torch.Tensor):
         """End-to-end step on HOST tensors (pinned preferred); synchronises."""
-        for t, shape, dt in ((actions, (self.n,), torch.uint8), (obs, (self.n, 7, 7, 3), torch.uint8),
+        for t, shape, dt in ((actions, (self.n,), torch.uint8), (obs, (self.n, *self.obs_shape), torch.uint8),
                              (reward, (self.n,), torch.float32), (terminated, (self.n,), torch.uint8),
                              (truncated, (self.n,), torch.uint8)):
             if t.device.type != "cpu" or t.dtype != dt or tuple(t.shape) != shape or not t.is_contiguous():
