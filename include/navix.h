@@ -149,6 +149,22 @@ NAVIX_API navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64
  * Host only, takes effect for subsequently enqueued steps. */
 NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost);
 
+/* Reward / termination function selection (Table 6 / Table 7, P:566-589;
+ * Code 4 `compose`; R#42).  Every family's events are exclusive:
+ *   NAVIX_EVENT_GOAL    (1) the goal / success event: on_goal_reached, and the
+ *                           family's success (KeyCorridor ball pickup, GoToDoor
+ *                           door: on_door_done in the navix reward mode)
+ *   NAVIX_EVENT_LAVA    (2) on_lava_fall
+ *   NAVIX_EVENT_FAILURE (4) Dynamic-Obstacles collision (R_3), GoToDoor's
+ *                           toggle / done away from the target ([MG])
+ * reward_events selects the events that pay their reward (else 0; 0 = the
+ * `free` reward function); termination_events the events that end the
+ * episode (0 = `free`: only truncation ends episodes; an event that does not
+ * terminate is not counted in the statistics).  Default 7 / 7 (Table 9's
+ * R_1 / R_2 / R_3).  Composes with navix_set_reward_costs.  Host only. */
+enum { NAVIX_EVENT_GOAL = 1, NAVIX_EVENT_LAVA = 2, NAVIX_EVENT_FAILURE = 4 };
+NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_events, uint32_t termination_events);
+
 /* Observation kinds (Table 5; R#41).  SYMBOLIC (the
  * default): first-person records uint8[7][7][3] = 147 B (symbolic_first_person)
  * and full grids uint8[W][H][3] (symbolic).  CATEGORICAL: the entity type

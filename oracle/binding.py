@@ -58,6 +58,7 @@ def oracle_lib():
     lib.oracle_process_vis7.argtypes = [P, P]
     lib.oracle_view_tags.argtypes = [I32, I32, I32, I32, I32, P]
     lib.oracle_set_reward_costs.argtypes = [P, ctypes.c_float, ctypes.c_float]
+    lib.oracle_set_event_functions.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32]
     lib.oracle_observe_full.argtypes = [P, P]
     lib.oracle_success_reward.argtypes = [I32, I32, I32]
     lib.oracle_success_reward.restype = ctypes.c_float
@@ -172,6 +173,9 @@ class OracleEnv:
 
     def set_reward_costs(self, time_cost: float, action_cost: float) -> None:
         self.lib.oracle_set_reward_costs(self.h, time_cost, action_cost)
+
+    def set_event_functions(self, reward_events: int, termination_events: int) -> None:
+        self.lib.oracle_set_event_functions(self.h, reward_events, termination_events)
 
     def observe_full(self) -> np.ndarray:
         s = self.spec

@@ -83,6 +83,11 @@ void oracle_observe(void* hp, uint8_t* obs) {
   for (size_t i = 0; i < h->envs.size(); ++i) h->envs[i].gen_obs(obs + i * 147);
 }
 
+void oracle_set_event_functions(void* hp, uint32_t reward_events, uint32_t termination_events) {
+  Handle* h = (Handle*)hp;
+  for (auto& e : h->envs) { e.reward_events = reward_events; e.termination_events = termination_events; }
+}
+
 void oracle_set_reward_costs(void* hp, float time_cost, float action_cost) {
   Handle* h = (Handle*)hp;
   for (auto& e : h->envs) { e.time_cost = time_cost; e.action_cost = action_cost; }

@@ -450,6 +450,18 @@ StepOut Env::step(int action) {
     collision = true;
     success = false;
   }
+  // Table 6 / Table 7 function selection (R#42): the events are exclusive;
+  // a deselected reward function pays 0, a deselected termination function
+  // does not end the episode (and the event is not counted in the statistics)
+  {
+    const bool fail_ev = collision || failure;
+    const uint32_t ev = success ? 1u : fail_ev ? 4u : lava ? 2u : 0u;  // [MG]: the collision override wins
+    if (ev && !(reward_events & ev)) reward = 0.f;
+    if (ev && !(termination_events & ev)) {
+      terminated = false;
+      success = lava = collision = failure = false;
+    }
+  }
   bool truncated = (step_count >= S.max_steps) && !terminated;  // R#17
   // Code 4 `compose` of the event reward with time_cost (every step) and
   // action_cost (every action but done), summed in binary32 in this order (R#31)

@@ -128,6 +128,10 @@ struct Env {
   Spec spec;
   int reward_mode = RM_MINIGRID;
   float time_cost = 0.f, action_cost = 0.f;  // Table 6 time_cost / action_cost (R#31)
+  // Table 6 / Table 7 selection (R#42): which events pay their reward and
+  // which end the episode; bit 0 the goal / success event, bit 1 lava, bit 2
+  // failure (collision, GoToDoor toggle / done away).  0 = `free`.
+  uint32_t reward_events = 7, termination_events = 7;
   uint64_t seed = 0;
   uint32_t global_index = 0;  // c0 of every Philox counter (shard invariance)
   Grid grid{1, 1};

@@ -32,6 +32,7 @@ struct navix_env {
   int device;
   int reward_mode;
   int obs_kind = 0;  // ObsKind (navix_set_observation)
+  uint32_t reward_events = 7, termination_events = 7;  // navix_set_event_functions (R#42)
   float time_cost = 0.f, action_cost = 0.f;
   uint8_t* state;
   bool owns_state;
@@ -154,6 +155,8 @@ KernelArgs make_args(navix_env* h) {
   a.action_cost = h->action_cost;
   a.gen_param = h->cfg.gen_param;
   a.obs_kind = h->obs_kind;
+  a.reward_events = h->reward_events;
+  a.termination_events = h->termination_events;
   return a;
 }
 
@@ -332,6 +335,15 @@ navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_
     return fail(NAVIX_E_INVALID_ARG, "reward costs must be finite and >= 0");
   h->time_cost = time_cost;
   h->action_cost = action_cost;
+  return NAVIX_OK;
+}
+
+navix_status navix_set_event_functions(navix_env* h, uint32_t reward_events, uint32_t termination_events) {
+  if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_event_functions: null handle");
+  if ((reward_events | termination_events) & ~7u)
+    return fail(NAVIX_E_INVALID_ARG, "event masks use bits 0-2 only (got %#x, %#x)", reward_events, termination_events);
+  h->reward_events = reward_events;
+  h->termination_events = termination_events;
   return NAVIX_OK;
 }
 

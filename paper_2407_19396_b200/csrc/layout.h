@@ -130,6 +130,7 @@ struct KernelArgs {
   int64_t rollout_steps;  // K of navix_rollout
   int gen_param;        // EnvConfig::gen_param (runtime level-generator parameter)
   int obs_kind;         // ObsKind of the obs outputs
+  uint32_t reward_events, termination_events;  // Table 6 / 7 selection (R#42): bit 0 success, 1 lava, 2 failure
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };

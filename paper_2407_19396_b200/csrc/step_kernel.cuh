@@ -367,7 +367,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       ax = (is_fwd && walk) ? fx : ax;
       ay = (is_fwd && walk) ? fy : ay;
       bool success = is_fwd && kind == K_GOAL;
-      const bool lava = is_fwd && kind == K_LAVA;
+      bool lava = is_fwd && kind == K_LAVA;
       bool coll = false;
       const bool pick = is_pick && ((0xE0u >> kind) & 1u) && carry == CELL_EMPTY;  // key, ball, box
       const bool drop = is_drop && fc == CELL_EMPTY && carry != CELL_EMPTY;
@@ -400,10 +400,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         success = success || (act == 6 && hit);
         coll = gtd_end && !success;  // counted as n_failure, reward 0
       }
-      // ---- a5: reward and termination (Eq. 1, Tables 6-7)
-      if (coll && FAM != FAM_GOTODOOR) reward = -1.0f;
-      else if (__builtin_expect(success, 0)) reward = success_reward(a.reward_mode, sc, C::T);
-      else if (lava) reward = a.reward_mode == 1 ? -1.0f : 0.0f;
+      // ---- a5: reward and termination (Eq. 1, Tables 6-7).
+      // The events are exclusive; the Table 6 / 7 selection (R#42) decides
+      // which of them pay their reward and which end the episode.
+      const uint32_t ev = success ? 1u : coll ? 4u : lava ? 2u : 0u;  // a collision into lava counts as collision
+      const uint32_t pay = ev & a.reward_events;
+      if (pay == 4u && FAM != FAM_GOTODOOR) reward = -1.0f;
+      else if (__builtin_expect(pay == 1u, 0)) reward = success_reward(a.reward_mode, sc, C::T);
+      else if (pay == 2u) reward = a.reward_mode == 1 ? -1.0f : 0.0f;
+      if (!(ev & a.termination_events)) success = lava = coll = false;
       // Code 4 `compose`: + (-time_cost) every step, + (-action_cost) for every
       // action but done, in binary32 in this order (R#31)
       if (a.time_cost != 0.f || a.action_cost != 0.f) {

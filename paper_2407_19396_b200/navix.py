@@ -27,7 +27,8 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
                 "n_lava", "n_failure", "n_truncated", "gen_failures")
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
-    "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
+    "navix_set_event_functions", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -80,6 +81,7 @@ def load_library():
         "navix_observe_full": ([P, P, P], I32),
         "navix_set_reward_costs": ([P, ctypes.c_float, ctypes.c_float], I32),
         "navix_set_observation": ([P, I32], I32),
+        "navix_set_event_functions": ([P, ctypes.c_uint32, ctypes.c_uint32], I32),
         "navix_sample_actions": ([P, U64, I64, I64, P, P], I32),
         "navix_step_host": ([P, P, P, P, P, P, P], I32),
         "navix_stats": ([P, P, P], I32),
@@ -223,6 +225,10 @@ class NavixEnv:
     def set_reward_costs(self, time_cost: float = 0.0, action_cost: float = 0.0) -> None:
         """Compose -time_cost per step and -action_cost per non-done action (Table 6)."""
         _check(self.lib.navix_set_reward_costs(self.h, time_cost, action_cost))
+
+    def set_event_functions(self, reward_events: int = 7, termination_events: int = 7) -> None:
+        """Table 6 / 7 selection: bit 0 goal/success, 1 lava, 2 failure; 0 = `free`."""
+        _check(self.lib.navix_set_event_functions(self.h, reward_events, termination_events))
 
     def observe_full(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """Table 5 `symbolic`: uint8[n, width, height, 3], agent cell (10, 0, dir)

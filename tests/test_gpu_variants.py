@@ -60,3 +60,31 @@ def test_full_obs_parity(env_id, nob):
         g.step(torch.from_numpy(acts[t]).cuda())
         o.step(acts[t])
     np.testing.assert_array_equal(g.observe_full().cpu().numpy(), o.observe_full())
+
+
+@pytest.mark.parametrize("env_id,mode,rev,tev", [("DoorKey-8x8-v0", 0, 0, 7), ("Empty-5x5-v0", 0, 7, 0),
+                                                 ("LavaGapS7-v0", 1, 5, 3), ("Dynamic-Obstacles-8x8-v0", 0, 7, 3),
+                                                 ("GoToDoor-8x8-v0", 0, 7, 1), ("KeyCorridorS3R3-v0", 1, 1, 6),
+                                                 ("Dynamic-Obstacles-8x8-v0", 1, 0, 0)])
+def test_event_functions_parity(env_id, mode, rev, tev):
+    # Table 6 / 7 selection incl. `free` (R#42), step and rollout paths, with costs composed
+    from paper_2407_19396_b200 import NavixEnv
+    n, K = 600, 300
+    g = NavixEnv(env_id, n, seed=3, reward_mode=mode)
+    r = NavixEnv(env_id, n, seed=3, reward_mode=mode)
+    o = OracleEnv(env_id, n, seed=3, reward_mode=mode)
+    for e in (g, r, o):
+        e.set_event_functions(rev, tev)
+        e.set_reward_costs(0.01, 0.0)
+        e.reset()
+    acts = random_actions(12, K, n, 0, high=8)
+    ro, rr, rte, rtr = r.rollout(torch.from_numpy(acts).cuda())
+    for t in range(K):
+        go, gr, gte, gtr = g.step(torch.from_numpy(acts[t]).cuda())
+        oo, orw, ote, otr = o.step(acts[t])
+        assert np.array_equal(gr.cpu().numpy().view(np.uint32), orw.view(np.uint32)), t
+        assert np.array_equal(rr[t].cpu().numpy().view(np.uint32), orw.view(np.uint32)), t
+        assert np.array_equal(gte.cpu().numpy(), ote) and np.array_equal(gtr.cpu().numpy(), otr), t
+        assert np.array_equal(go.cpu().numpy(), oo), t
+    np.testing.assert_array_equal(g.stats().cpu().numpy(), o.stats())
+    np.testing.assert_array_equal(g.export_state(), o.export())

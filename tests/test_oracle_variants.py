@@ -82,3 +82,54 @@ def test_full_obs_doorkey_layout_and_carry_not_drawn():
     env.step(np.array([3], np.uint8))              # pick up the key
     full = env.observe_full()[0]
     assert full[1, 2].tolist() == [10, 0, 1] and full[1, 3].tolist() == [1, 0, 0]
+
+
+def _walk_empty5(actions, reward_events, termination_events):
+    env = OracleEnv("Empty-5x5-v0", 1)
+    env.reset()
+    env.set_event_functions(reward_events, termination_events)
+    return env, [env.step(np.array([a], np.uint8))[1:] for a in actions]
+
+
+def test_event_functions_free_reward_and_free_termination():
+    # Table 6 / 7 `free` (R#42).  Empty-5x5 from (1,1) east: F (2,1), F (3,1),
+    # R (south), F (3,2), F (3,3) = the goal at step 5
+    path = [2, 2, 1, 2, 2]
+    env, out = _walk_empty5(path, 7, 7)
+    assert out[-1][1][0] == 1 and out[-1][0][0] == np.float32(1 - 0.9 * 5 / 100)
+    env, out = _walk_empty5(path, 0, 7)             # free reward: the goal still terminates
+    assert out[-1][1][0] == 1 and out[-1][0][0] == 0.0
+    env, out = _walk_empty5(path, 7, 0)             # free termination: paid, not terminated
+    assert out[-1][1][0] == 0 and out[-1][0][0] == np.float32(1 - 0.9 * 5 / 100)
+    st = env.stats()
+    assert st[0] == 0                              # no episode ended
+    # standing on the goal does not pay again; walking off and back on does
+    _, r, te, tr = env.step(np.array([0], np.uint8))
+    assert r[0] == 0 and te[0] == 0
+    for _ in range(100 - 6 - 1):
+        _, r, te, tr = env.step(np.array([0], np.uint8))
+    _, r, te, tr = env.step(np.array([0], np.uint8))
+    assert tr[0] == 1 and te[0] == 0                # only truncation ends it
+    st = env.stats()
+    assert st[0] == 1 and st[2] == 0 and st[6] == 1
+
+
+def test_event_functions_lava_and_collision():
+    # LavaGap navix mode: lava pays -1 unless deselected; DynObs collision continues if not terminating
+    from inputgen import record_from_map
+    rows = ["#######", "#.A.V.#", "#.....#", "#.....#", "#.....#", "#....G#", "#######"]
+    for rev, tev, want in ((7, 7, (-1.0, 1)), (5, 7, (0.0, 1)), (7, 5, (-1.0, 0)), (0, 0, (0.0, 0))):
+        env = OracleEnv("LavaGapS7-v0", 1, reward_mode=1)
+        env.reset()
+        env.import_(record_from_map(rows, 0).reshape(1, -1))
+        env.set_event_functions(rev, tev)
+        env.step(np.array([2], np.uint8))
+        _, r, te, _ = env.step(np.array([2], np.uint8))   # onto the lava at (4,1)
+        assert (float(r[0]), int(te[0])) == want, (rev, tev)
+    env = OracleEnv("Dynamic-Obstacles-5x5", 1)
+    env.reset()
+    env.set_event_functions(7, 3)                          # collisions pay -1 but do not end the episode
+    env.import_(record_from_map(["#####", "#A..#", "#..B#", "#.BG#", "#####"], 3,
+                                balls=[(3, 2), (2, 3)]).reshape(1, -1))  # facing the wall north
+    _, r, te, _ = env.step(np.array([2], np.uint8))
+    assert r[0] == -1.0 and te[0] == 0
