@@ -298,12 +298,23 @@ def run_navix(args, rank, world, local_rank):
         r1.record(s)
         torch.cuda.synchronize(dev)
         t_r = max_over_ranks(r0.elapsed_time(r1) / 1e3 / reps, dev)
+        # the same K steps with the random policy drawn inside the kernel (no action reads)
+        env.rollout_random(1, 0, Kr, out=outs)
+        barrier()
+        r0.record(s)
+        for _ in range(reps):
+            env.rollout_random(1, 0, Kr, out=outs)
+        r1.record(s)
+        torch.cuda.synchronize(dev)
+        t_rr = max_over_ranks(r0.elapsed_time(r1) / 1e3 / reps, dev)
         Br = 1 + 147 + 4 + 2
         rollout = {"steps_per_launch": Kr, "value": n_total * Kr / t_r, "unit": UNIT,
                    "ms_per_launch": 1e3 * t_r, "algorithmic_bytes_per_env_step": Br,
                    "achieved_GBps_per_gpu": Br * n * Kr / t_r / 1e9,
                    "frac_of_measured_hbm": Br * n * Kr / t_r / 1e9 / measured_peaks()[0],
-                   "api": "navix_rollout (state on chip across the K steps; row f1)"}
+                   "api": "navix_rollout (state on chip across the K steps; row f1)",
+                   "in_kernel_policy": {"value": n_total * Kr / t_rr, "unit": UNIT, "ms_per_launch": 1e3 * t_rr,
+                                        "api": "navix_rollout_random (Philox policy inside the kernel)"}}
         del outs
 
     # f3: the same step emitting Table 5 `categorical_first_person` (49 B records)

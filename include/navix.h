@@ -142,6 +142,16 @@ NAVIX_API navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t*
 NAVIX_API navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, uint8_t* obs,
                                      float* reward, uint8_t* terminated, uint8_t* truncated, void* stream);
 
+/* navix_rollout with the uniform random policy drawn inside the kernel
+ * (SURVEY §8f row f1): the action of env i at step t is the one
+ * navix_sample_actions(action_seed, t0 + t) writes (Philox key action_seed,
+ * counter (global env index, t0 + t, 2 << 16, 0), word 0, bounded by
+ * n_actions), so the results equal navix_rollout on those sampled actions.
+ * No action buffer is read.  Outputs as navix_rollout. */
+NAVIX_API navix_status navix_rollout_random(navix_env* h, uint64_t action_seed, int64_t t0, int64_t steps,
+                                            uint8_t* obs, float* reward, uint8_t* terminated, uint8_t* truncated,
+                                            void* stream);
+
 /* Reward composition (Table 6 `time_cost`, `action_cost`; Code 4 `compose`,
  * P:673-680; R#31): every later step adds -time_cost, and
  * -action_cost unless the action is done (6), to the event reward, in binary32

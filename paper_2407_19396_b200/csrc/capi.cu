@@ -329,6 +329,25 @@ navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, 
   return launch(h, MODE_ROLLOUT, a, stream);
 }
 
+navix_status navix_rollout_random(navix_env* h, uint64_t action_seed, int64_t t0, int64_t steps, uint8_t* obs,
+                                  float* reward, uint8_t* terminated, uint8_t* truncated, void* stream) {
+  if (!h || !obs || !reward || !terminated || !truncated)
+    return fail(NAVIX_E_INVALID_ARG, "navix_rollout_random: null argument");
+  if (steps <= 0 || t0 < 0)
+    return fail(NAVIX_E_INVALID_ARG, "navix_rollout_random: steps must be positive and t0 >= 0");
+  KernelArgs a = make_args(h);
+  a.actions = nullptr;  // in-kernel policy
+  a.act_key_lo = (uint32_t)action_seed;
+  a.act_key_hi = (uint32_t)(action_seed >> 32);
+  a.act_t0 = (uint32_t)t0;
+  a.obs = obs;
+  a.reward = reward;
+  a.terminated = terminated;
+  a.truncated = truncated;
+  a.rollout_steps = steps;
+  return launch(h, MODE_ROLLOUT, a, stream);
+}
+
 navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost) {
   if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_reward_costs: null handle");
   if (!(time_cost >= 0.f && time_cost < 1e30f) || !(action_cost >= 0.f && action_cost < 1e30f))

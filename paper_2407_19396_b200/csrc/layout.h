@@ -131,6 +131,9 @@ struct KernelArgs {
   int gen_param;        // EnvConfig::gen_param (runtime level-generator parameter)
   int obs_kind;         // ObsKind of the obs outputs
   uint32_t reward_events, termination_events;  // Table 6 / 7 selection (R#42): bit 0 success, 1 lava, 2 failure
+  // rollout with actions == nullptr: in-kernel uniform random policy, the
+  // navix_sample_actions stream (key act_key, counter (env, act_t0 + t, 2 << 16, 0))
+  uint32_t act_key_lo, act_key_hi, act_t0;
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };

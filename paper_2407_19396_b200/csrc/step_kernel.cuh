@@ -663,10 +663,18 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   mbar_wait(mbar, 0);
   EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
   bool dirty = false;
-  uint32_t next_act = valid ? a.actions[e] : 0u;
+  // actions from actions[t][n], or drawn in-kernel from the random-policy
+  // stream (the one navix_sample_actions writes: bit-identical results)
+  const bool draw = a.actions == nullptr;
+  const uint32_t genv = a.env_begin + (uint32_t)e;
+  auto policy = [&](int64_t t) -> uint32_t {
+    const uint4 w = philox4x32_10(make_uint4(genv, a.act_t0 + (uint32_t)t, 2u << 16, 0u), a.act_key_lo, a.act_key_hi);
+    return bounded(w.x, (uint32_t)C::NA);
+  };
+  uint32_t next_act = !valid ? 0u : draw ? policy(0) : a.actions[e];
   for (int64_t t = 0; t < K; ++t) {
     in.act = next_act;
-    if (t + 1 < K && valid) next_act = a.actions[(t + 1) * a.n + e];  // one step ahead
+    if (t + 1 < K && valid) next_act = draw ? policy(t + 1) : a.actions[(t + 1) * a.n + e];  // one step ahead
     KernelArgs as = a;
     as.obs = a.obs + t * a.n * obs_record_bytes(OBSK);
     as.reward = a.reward + t * a.n;

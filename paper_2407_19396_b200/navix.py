@@ -28,7 +28,7 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
-    "navix_set_event_functions", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_set_event_functions", "navix_rollout_random", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -78,6 +78,7 @@ def load_library():
         "navix_step": ([P, P, P, P, P, P, P], I32),
         "navix_observe": ([P, P, P], I32),
         "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
+        "navix_rollout_random": ([P, U64, I64, I64, P, P, P, P, P], I32),
         "navix_observe_full": ([P, P, P], I32),
         "navix_set_reward_costs": ([P, ctypes.c_float, ctypes.c_float], I32),
         "navix_set_observation": ([P, I32], I32),
@@ -220,6 +221,25 @@ class NavixEnv:
         self._check_out(trunc, (K, self.n), torch.uint8)
         _check(self.lib.navix_rollout(self.h, _ptr(actions), K, _ptr(obs), _ptr(rew), _ptr(term), _ptr(trunc),
                                       _stream(dev)))
+        return obs, rew, term, trunc
+
+    def rollout_random(self, action_seed: int, t0: int, steps: int, out=None):
+        """K steps in one launch under the in-kernel uniform random policy
+        (the sample_actions(action_seed, t0, K) stream); outputs as rollout()."""
+        K = int(steps)
+        dev = self.device
+        if out is None:
+            out = (torch.empty((K, self.n, *self.obs_shape), dtype=torch.uint8, device=dev),
+                   torch.empty((K, self.n), dtype=torch.float32, device=dev),
+                   torch.empty((K, self.n), dtype=torch.uint8, device=dev),
+                   torch.empty((K, self.n), dtype=torch.uint8, device=dev))
+        obs, rew, term, trunc = out
+        self._check_out(obs, (K, self.n, *self.obs_shape), torch.uint8)
+        self._check_out(rew, (K, self.n), torch.float32)
+        self._check_out(term, (K, self.n), torch.uint8)
+        self._check_out(trunc, (K, self.n), torch.uint8)
+        _check(self.lib.navix_rollout_random(self.h, action_seed & (2 ** 64 - 1), t0, K, _ptr(obs), _ptr(rew),
+                                             _ptr(term), _ptr(trunc), _stream(dev)))
         return obs, rew, term, trunc
 
     def set_reward_costs(self, time_cost: float = 0.0, action_cost: float = 0.0) -> None:

@@ -52,3 +52,19 @@ def test_rollout_matches_oracle():
         assert np.array_equal(rte[t].cpu().numpy(), ote) and np.array_equal(rtr[t].cpu().numpy(), otr)
     assert np.array_equal(g.export_state(), o.export())
     assert np.array_equal(g.stats().cpu().numpy(), o.stats())
+
+
+@pytest.mark.parametrize("env_id,n,K,t0", [("DoorKey-8x8-v0", 1000, 50, 0), ("Dynamic-Obstacles-8x8-v0", 513, 40, 7),
+                                          ("KeyCorridorS3R3-v0", 300, 30, 123), ("FourRooms-v0", 200, 30, 5)])
+def test_rollout_random_policy_in_kernel(env_id, n, K, t0):
+    # row f1: the in-kernel random policy equals rollout() on sample_actions()'s stream
+    from paper_2407_19396_b200 import NavixEnv
+    a = NavixEnv(env_id, n, seed=4)
+    b = NavixEnv(env_id, n, seed=4)
+    a.reset()
+    b.reset()
+    ra = a.rollout_random(77, t0, K)
+    rb = b.rollout(b.sample_actions(77, t0, K))
+    for x, y in zip(ra, rb):
+        assert torch.equal(x, y)
+    np.testing.assert_array_equal(a.export_state(), b.export_state())
