@@ -600,9 +600,16 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     if (t < n_tiles) issue_tile_loads<FAM, H * C::RW, MODE_STEP>(a, t, s_buf[k], smem_u32(&s_mbar[k]));
     else mbar_arrive(smem_u32(&s_mbar[k]));
   };
+  // Programmatic dependent launch: let the next step's grid be scheduled now
+  // (its CTAs take the SM slots ours free and wait below), and wait for the
+  // previous step's grid to complete and flush before touching global memory.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid == 0) {
     mbar_init(smem_u32(&s_mbar[0]), 1);
     mbar_init(smem_u32(&s_mbar[1]), 1);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) {
     publish(0, atomicAdd(&sched[0], 1u));
     publish(1, atomicAdd(&sched[0], 1u));
   }
@@ -806,7 +813,24 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       }
       const int64_t cap = (int64_t)per_sm * n_sm;
       const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
-      navix_step_persistent<FAM, H, W, OBSK><<<grid, block, 0, s>>>(a);
+      // launched with programmatic stream serialization (PDL): back-to-back
+      // steps overlap the launch of step t+1 with the tail of step t
+      static int pdl = -1;
+      if (pdl < 0) {
+        const char* v = getenv("NAVIX_PDL");
+        pdl = !(v && v[0] == '0');
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = block;
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl ? 1 : 0;
+      return cudaLaunchKernelEx(&cfg, navix_step_persistent<FAM, H, W, OBSK>, a);
     }
   } else if (mode == MODE_FULL_OBS) {
     full_obs_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
