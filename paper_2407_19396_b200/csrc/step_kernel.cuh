@@ -811,7 +811,13 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE, 0);
         if (per_sm < 1) per_sm = 1;
       }
-      const int64_t cap = (int64_t)per_sm * n_sm;
+      int64_t cap = (int64_t)per_sm * n_sm;
+      static int64_t ctas_env = -1;
+      if (ctas_env < 0) {
+        const char* v = getenv("NAVIX_PERSIST_CTAS");  // experiment switch: persistent grid size
+        ctas_env = v ? atoll(v) : 0;
+      }
+      if (ctas_env > 0) cap = ctas_env;
       const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
       // launched with programmatic stream serialization (PDL): back-to-back
       // steps overlap the launch of step t+1 with the tail of step t
