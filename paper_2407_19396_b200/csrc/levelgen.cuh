@@ -14,7 +14,7 @@ namespace navix {
 template <int FAM, int H, int W>
 struct Cfg {
   static constexpr int RW = (W + 7) / 8;             // u64 planes per grid row (f2: 16- / 24-byte rows)
-  static constexpr int NPL = RW == 1 ? 8 : RW == 2 ? 32 : RW * H;  // SMEM planes per env (8 lines / 16 rows x 2 / H x RW)
+  static constexpr int NPL = RW == 1 ? 8 : RW * H;  // SMEM planes per env (8 lines / H rows x RW)
   static constexpr int RS = (W - 1) / 3 + 1;         // KeyCorridor room size (3 columns of rooms)
   static constexpr int NR = (H - 1) / (RS - 1);      // KeyCorridor rows
   static constexpr int T = FAM == FAM_DOORKEY ? 10 * W * W

@@ -212,48 +212,7 @@ __device__ __forceinline__ void view_columns_narrow(const uint64_t* lines, int a
   }
 }
 
-// The same for grids up to 16x16 (row f2): `rows` holds 16 rows of 16 bytes
-// as two u64 planes per row (plane 2y + h at rows[(2y + h) * TILE]); even
-// directions read a 7-byte window of one row (3 word loads, 2 funnel shifts,
-// 2 permutes to reverse), odd directions gather one byte per row from 7 rows.
-__device__ __forceinline__ uint32_t row_word(const uint64_t* rows, int y, int k) {
-  // word k (bytes 4k..4k+3) of row y, both taken mod 16 / mod 4
-  return reinterpret_cast<const uint32_t*>(rows + ((2 * (y & 15) + ((k >> 1) & 1)) * TILE))[k & 1];
-}
-__device__ __forceinline__ void view_columns_wide(const uint64_t* rows, int ax, int ay, int dir, uint32_t (&clo)[7],
-                                                  uint32_t (&chi)[7]) {
-  const int base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
-  const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
-  const int s = (dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6) & 15;  // first position of the window
-  const bool rev = dir <= 1;
-  if ((dir & 1) == 0) {
-    const int q = s >> 2, r = 8 * (s & 3);
-#pragma unroll
-    for (int vi = 0; vi < 7; ++vi) {
-      const int y = base + sgn * vi;
-      const uint32_t w0 = row_word(rows, y, q), w1 = row_word(rows, y, q + 1), w2 = row_word(rows, y, q + 2);
-      const uint32_t f_lo = __funnelshift_r(w0, w1, r), f_hi = __funnelshift_r(w1, w2, r);
-      clo[vi] = rev ? prmt(f_lo, f_hi, 0x3456u) : f_lo;
-      chi[vi] = rev ? prmt(f_lo, f_hi, 0x0012u) : f_hi;
-    }
-  } else {
-#pragma unroll
-    for (int vi = 0; vi < 7; ++vi) {
-      const int x = (base + sgn * vi) & 15;
-      const uint32_t xb = (uint32_t)(x & 3), pair = ((4u + xb) << 4) | xb;
-      uint32_t w[7];
-#pragma unroll
-      for (int k = 0; k < 7; ++k) w[k] = row_word(rows, s + k, x >> 2);  // rows s .. s+6, byte x
-      const uint32_t p01 = prmt(w[0], w[1], pair), p23 = prmt(w[2], w[3], pair);
-      const uint32_t p45 = prmt(w[4], w[5], pair), p6 = prmt(w[6], w[6], pair);
-      const uint32_t f_lo = prmt(p01, p23, 0x5410u), f_hi = prmt(p45, p6, 0x5410u);  // cells y = s .. s+6
-      clo[vi] = rev ? prmt(f_lo, f_hi, 0x3456u) : f_lo;
-      chi[vi] = rev ? prmt(f_lo, f_hi, 0x0012u) : f_hi;
-    }
-  }
-}
-
-// The same for rows of RW >= 3 planes (grids wider than 16, FourRooms): row
+// The same for grids wider than 8 (RW >= 2 u64 planes per row, row f2): row
 // y is clamped into the grid and the window is read from the row with 8 zero
 // bytes prepended (virtual word w < 2 is 0), so every load stays inside this
 // env's H x RW planes; out-of-grid positions read arbitrary bytes (R#12).
@@ -463,22 +422,6 @@ __device__ __forceinline__ void observe_cols_cat(uint32_t (&clo)[7], uint32_t (&
     case 2: emit_cat_record<2>(out, t); break;
     default: emit_cat_record<3>(out, t); break;
   }
-}
-
-// Observation of one env on a grid up to 8x8 (lines: see view_columns_narrow).
-__device__ __forceinline__ void observe_emit(const uint64_t* lines, int ax, int ay, int dir, uint32_t carry,
-                                             uint32_t* out, int M) {
-  uint32_t clo[7], chi[7];
-  view_columns_narrow(lines, ax, ay, dir, clo, chi);
-  observe_cols(clo, chi, carry, out, M);
-}
-
-// Observation of one env on a grid up to 16x16 (rows: see view_columns_wide).
-__device__ __forceinline__ void observe_emit_wide(const uint64_t* rows, int ax, int ay, int dir, uint32_t carry,
-                                                  uint32_t* out, int M) {
-  uint32_t clo[7], chi[7];
-  view_columns_wide(rows, ax, ay, dir, clo, chi);
-  observe_cols(clo, chi, carry, out, M);
 }
 
 }  // namespace navix

@@ -458,7 +458,6 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     const int M = OBSK == OBS_CATEGORICAL ? warp & 3 : (3 * warp) & 3;
     uint32_t clo[7], chi[7];
     if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
-    else if constexpr (RW == 2) view_columns_wide(rows, ax, ay, dir, clo, chi);
     else view_columns_big<RW, H>(rows, ax, ay, dir, clo, chi);
     if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
     if constexpr (OBSK == OBS_CATEGORICAL) observe_cols_cat(clo, chi, carry, s32 + ((le * OB - M) >> 2), M);
@@ -582,13 +581,22 @@ __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const Kern
 // variant where the last warp to finish issues the store measured 1.3 % slower:
 // its warps spin on mbarriers instead.)  The last CTA to finish resets the
 // scheduler, so the kernel replays from a CUDA graph.
+template <int FAM, int NPL, int OBSK>
+struct PersistSmem {
+  uint8_t obs[TILE * obs_record_bytes(OBSK)];
+  TileSmem<FAM, NPL> buf[2];
+  uint64_t mbar[2];  // tile inputs landed (per buffer)
+  int64_t tile[2];
+};
+
 template <int FAM, int H, int W, int OBSK>
 __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
-  __shared__ __align__(128) uint8_t s_obs[TILE * obs_record_bytes(OBSK)];
   using C = Cfg<FAM, H, W>;
-  __shared__ __align__(128) TileSmem<FAM, C::NPL> s_buf[2];
-  __shared__ __align__(8) uint64_t s_mbar[2];   // tile inputs landed (per buffer)
-  __shared__ int64_t s_tile[2];
+  auto& S = *reinterpret_cast<PersistSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
+  uint8_t* const s_obs = S.obs;
+  auto& s_buf = S.buf;
+  auto& s_mbar = S.mbar;
+  auto& s_tile = S.tile;
   const int64_t n_tiles = (a.n + TILE - 1) / TILE;
   unsigned int* const sched = a.sched;          // [0] next tile, [1] CTAs done
   const int tid = threadIdx.x;
@@ -798,17 +806,22 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
     const char* v = getenv("NAVIX_STEP_KERNEL");  // experiment switch
     onetile = v && v[0] == 'o';
   }
-  if (mode == MODE_STEP && (onetile || W > 8)) {  // wide grids: one tile per CTA (SMEM)
+  // the persistent kernel double-buffers the tile inputs in SMEM: grids up
+  // to 24 row planes (e.g. 12 rows of 9-16 cells); larger ones run one tile per CTA
+  constexpr bool PERSIST = H * C::RW <= 24;
+  constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
+  if (mode == MODE_STEP && (onetile || !PERSIST)) {
     navix_kernel<FAM, H, W, MODE_STEP, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);
   } else if (mode == MODE_STEP) {
-    if constexpr (W <= 8) {
+    if constexpr (PERSIST) {
       // persistent grid: as many CTAs as fit on the device at once
       static int per_sm = -1, n_sm = -1;
       if (per_sm < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE, 0);
+        allow_dyn_smem(navix_step_persistent<FAM, H, W, OBSK>, PDYN);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE, PDYN);
         if (per_sm < 1) per_sm = 1;
       }
       int64_t cap = (int64_t)per_sm * n_sm;
@@ -829,7 +842,7 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = block;
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = PDYN;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

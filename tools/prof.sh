@@ -12,6 +12,6 @@ if [ "$MODE" = launches ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py $ARGS > /dev/null 2>&1; echo "launch list rc=$?"
 else
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-navix_step_persistent} -s 5 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-navix_step_persistent} -s ${SKIP:-5} -c 1 \
     -o gpurun_out/prof_$TAG python bench.py $ARGS > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
