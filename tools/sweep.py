@@ -13,6 +13,7 @@ import json
 import os
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,9 +42,20 @@ CONFIGS = [  # (env id, largest N) per BASELINE.json configs
     ("Dynamic-Obstacles-Random-6x6", 1 << 20),
 ]
 SIZES = [1, 8, 1 << 10, 1 << 11, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 21, 1 << 22, 1 << 23]
+# every Table 9 id at the paper's batch (2048), 2^16 and 2^20 envs
+CATALOG = ["Empty-5x5-v0", "Empty-6x6-v0", "Empty-8x8-v0", "Empty-16x16-v0", "Empty-Random-5x5", "Empty-Random-6x6",
+           "Empty-Random-8x8", "Empty-Random-16x16", "DoorKey-5x5-v0", "DoorKey-6x6-v0", "DoorKey-8x8-v0",
+           "DoorKey-16x16-v0", "DoorKey-Random-5x5", "DoorKey-Random-6x6", "DoorKey-Random-8x8",
+           "DoorKey-Random-16x16", "FourRooms-v0", "KeyCorridorS3R1-v0", "KeyCorridorS3R2-v0", "KeyCorridorS3R3-v0",
+           "KeyCorridorS4R3-v0", "KeyCorridorS5R3-v0", "KeyCorridorS6R3-v0", "LavaGapS5-v0", "LavaGapS6-v0",
+           "LavaGapS7-v0", "SimpleCrossingS9N1-v0", "SimpleCrossingS9N2-v0", "SimpleCrossingS9N3-v0",
+           "SimpleCrossingS11N5-v0", "Dynamic-Obstacles-5x5", "Dynamic-Obstacles-6x6", "Dynamic-Obstacles-8x8",
+           "Dynamic-Obstacles-16x16", "DistShift1-v0", "DistShift2-v0", "GoToDoor-5x5-v0", "GoToDoor-6x6-v0",
+           "GoToDoor-8x8-v0"]
+CATALOG_SIZES = [1 << 11, 1 << 16, 1 << 20]
 
 
-def time_point(env_id: str, n: int, steps: int, warmup: int = 10):
+def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5):
     env = NavixEnv(env_id, n, seed=0)
     env.reset()
     ring = min(steps, 256)
@@ -58,18 +70,23 @@ def time_point(env_id: str, n: int, steps: int, warmup: int = 10):
     g.replay()
     torch.cuda.synchronize()
     reps = max(1, steps // ring)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        g.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / (reps * ring)
+    times = []
+    for _ in range(runs):  # each point five times, 5/50/95 percentiles
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3 / (reps * ring))
+    t = float(np.percentile(times, 50))
     B = algorithmic_bytes(env.spec)
     peak, _ = measured_peaks()
     st = env.stats().cpu().tolist()
     env.close()
+    rates = sorted(n / x for x in times)
     return {"env": env_id, "n": n, "us_per_step": t * 1e6, "env_steps_per_s": n / t,
+            "env_steps_per_s_p5_p50_p95": [float(np.percentile(rates, q)) for q in (5, 50, 95)], "runs": runs,
             "GBps": B * n / t / 1e9, "frac_of_measured_hbm": B * n / t / 1e9 / peak, "bytes_per_env_step": B,
             "episodes": st[0]}
 
@@ -80,17 +97,22 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "sweep.json"))
     ap.add_argument("--sizes", default="", help="comma-separated batch sizes (default: the full list)")
     ap.add_argument("--envs", default="", help="comma-separated env ids (default: all)")
+    ap.add_argument("--runs", type=int, default=5, help="timed repetitions per point (percentiles)")
+    ap.add_argument("--catalog", action="store_true", help="every Table 9 id at 2^11 / 2^16 / 2^20 envs")
     a = ap.parse_args()
     rows = []
     sizes = [int(x) for x in a.sizes.split(",") if x] or SIZES
     envs = set(x for x in a.envs.split(",") if x)
-    for env_id, nmax in CONFIGS:
+    configs = [(e, 1 << 20) for e in CATALOG] if a.catalog else CONFIGS
+    if a.catalog and not a.sizes:
+        sizes = CATALOG_SIZES
+    for env_id, nmax in configs:
         if envs and env_id not in envs:
             continue
         for n in sizes:
             if n > nmax:
                 continue
-            r = time_point(env_id, n, a.steps)
+            r = time_point(env_id, n, a.steps, runs=a.runs)
             rows.append(r)
             print(f"{env_id:28s} N={n:>8d}  {r['us_per_step']:9.2f} us/step  {r['env_steps_per_s'] / 1e9:8.3f} G/s  "
                   f"{r['GBps']:7.0f} GB/s  {100 * r['frac_of_measured_hbm']:5.1f}%", flush=True)
