@@ -278,6 +278,15 @@ def run_navix(args, rank, world, local_rank):
 
     # episode statistics: the one collective of the path (NCCL all-reduce of int64[8])
     st = all_reduce_stats(env.stats()).cpu().numpy()
+    # its cost (once per report interval): stats reduction kernel +
+    # all-reduce, device-timed, against 100 steps
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(s)
+    for _ in range(10):
+        all_reduce_stats(env.stats())
+    s1.record(s)
+    torch.cuda.synchronize(dev)
+    t_stats = max_over_ranks(s0.elapsed_time(s1) / 1e3 / 10, dev)
 
     # f1: fused K-step rollout (navix_rollout), same envs and random policy
     rollout = None
@@ -396,6 +405,9 @@ def run_navix(args, rank, world, local_rank):
         "rollout": rollout,
         "categorical": categorical,
         "clocks": clk.summary(),
+        "stats_allreduce": {"us_per_call": 1e6 * t_stats,
+                            "frac_of_100_steps": t_stats / (100 * t_max / args.steps),
+                            "api": "navix_stats + torch.distributed all_reduce (NCCL for N > 1)"},
         "episode_stats": {k: int(v) for k, v in zip(
             ("episodes", "sum_len", "n_success", "sum_success_step", "n_lava", "n_failure", "n_truncated",
              "gen_failures"), st)},
