@@ -91,6 +91,30 @@ def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5)
             "episodes": st[0]}
 
 
+def time_rollout(env_id: str, n: int, K: int, runs: int = 5):
+    """Row f1: K steps per launch (navix_rollout_random), per-step time."""
+    env = NavixEnv(env_id, n, seed=0)
+    env.reset()
+    out = env.rollout_random(1, 0, K)  # warm-up, allocates the [K, n] outputs
+    torch.cuda.synchronize()
+    times = []
+    for r in range(runs):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        env.rollout_random(1, (r + 1) * K, K, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3 / K)
+    t = float(np.percentile(times, 50))
+    B = 1 + 147 + 4 + 2
+    peak, _ = measured_peaks()
+    env.close()
+    rates = sorted(n / x for x in times)
+    return {"env": env_id, "n": n, "rollout_k": K, "us_per_step": t * 1e6, "env_steps_per_s": n / t,
+            "env_steps_per_s_p5_p50_p95": [float(np.percentile(rates, q)) for q in (5, 50, 95)], "runs": runs,
+            "GBps": B * n / t / 1e9, "frac_of_measured_hbm": B * n / t / 1e9 / peak, "bytes_per_env_step": B}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=512)
@@ -99,6 +123,7 @@ def main():
     ap.add_argument("--envs", default="", help="comma-separated env ids (default: all)")
     ap.add_argument("--runs", type=int, default=5, help="timed repetitions per point (percentiles)")
     ap.add_argument("--catalog", action="store_true", help="every Table 9 id at 2^11 / 2^16 / 2^20 envs")
+    ap.add_argument("--rollout-k", type=int, default=0, help="time navix_rollout_random with K steps per launch")
     a = ap.parse_args()
     rows = []
     sizes = [int(x) for x in a.sizes.split(",") if x] or SIZES
@@ -112,7 +137,12 @@ def main():
         for n in sizes:
             if n > nmax:
                 continue
-            r = time_point(env_id, n, a.steps, runs=a.runs)
+            if a.rollout_k:
+                if n * a.rollout_k * 147 > (24 << 30):
+                    continue
+                r = time_rollout(env_id, n, a.rollout_k, runs=a.runs)
+            else:
+                r = time_point(env_id, n, a.steps, runs=a.runs)
             rows.append(r)
             print(f"{env_id:28s} N={n:>8d}  {r['us_per_step']:9.2f} us/step  {r['env_steps_per_s'] / 1e9:8.3f} G/s  "
                   f"{r['GBps']:7.0f} GB/s  {100 * r['frac_of_measured_hbm']:5.1f}%", flush=True)
