@@ -325,11 +325,21 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
               m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (4 * dy);
             }
           } else {
+            // wide rows: the 3 cells x = bx-1 .. bx+1 of a row from one or two
+            // 32-bit words (a funnel shift), then the same SWAR empty test
+            const int x0 = bx - 1, k = x0 >> 2, sh = 8 * (x0 & 3);
 #pragma unroll
-            for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx)
-                m |= (g.get(bx - 1 + dx, by - 1 + dy) == CELL_EMPTY ? 1u : 0u) << (4 * dy + dx);
+            for (int dy = 0; dy < 3; ++dy) {
+              const int y = by - 1 + dy;
+              const uint32_t* w = reinterpret_cast<const uint32_t*>(rows + (y * RW + (k >> 1)) * TILE) + (k & 1);
+              const uint32_t w0 = *w;
+              const uint32_t* w1p = reinterpret_cast<const uint32_t*>(rows + (y * RW + ((k + 1) >> 1)) * TILE) +
+                                    ((k + 1) & 1);
+              const uint32_t w1 = (x0 & 3) > 1 ? *w1p : 0u;  // only when the 3 cells straddle two words
+              const uint32_t x = (__funnelshift_r(w0, w1, sh) & 0x00FFFFFFu) ^ 0x01010101u;
+              const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
+              m |= (((z & 0x00808080u) * 0x00204080u) >> 28) << (4 * dy);
+            }
           }
           const int adx = ax - (bx - 1), ady = ay - (by - 1);
           if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (4 * ady + adx));
