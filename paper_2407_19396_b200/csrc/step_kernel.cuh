@@ -628,8 +628,10 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (tid == 0) {
-    publish(0, atomicAdd(&sched[0], 1u));
-    publish(1, atomicAdd(&sched[0], 1u));
+    // the first two tiles are static (b, b + grid): no burst of contended
+    // atomics on the scheduler word when every CTA starts at once
+    publish(0, (int64_t)blockIdx.x);
+    publish(1, (int64_t)blockIdx.x + gridDim.x);
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     if (tile >= n_tiles) break;
     // claim the tile-after-next now: the atomic's latency hides behind the compute
     unsigned int next = 0;
-    if (tid == 0) next = atomicAdd(&sched[0], 1u);
+    if (tid == 0) next = atomicAdd(&sched[0], 1u) + 2u * gridDim.x;
     const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK>(
         a, tile, &s_buf[cur].rows[0][tid], nullptr, decode_staged<FAM, MODE_STEP>(a, tile, s_buf[cur]), s_obs, [&] {
       if (it > 0) {  // the previous tile's store must have read s_obs
