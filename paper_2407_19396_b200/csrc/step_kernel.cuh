@@ -622,6 +622,9 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   // (its CTAs take the SM slots ours free and wait below), and wait for the
   // previous step's grid to complete and flush before touching global memory.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // small batches (<= 4 tiles per CTA): plain striding, no scheduler atomics
+  // on the critical path; larger ones balance with the atomic counter
+  const bool stride_only = n_tiles <= 4 * (int64_t)gridDim.x;
   if (tid == 0) {
     mbar_init(smem_u32(&s_mbar[0]), 1);
     mbar_init(smem_u32(&s_mbar[1]), 1);
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     if (tile >= n_tiles) break;
     // claim the tile-after-next now: the atomic's latency hides behind the compute
     unsigned int next = 0;
-    if (tid == 0) next = atomicAdd(&sched[0], 1u) + 2u * gridDim.x;
+    if (tid == 0) next = stride_only ? (unsigned)(tile + 2 * gridDim.x) : atomicAdd(&sched[0], 1u) + 2u * gridDim.x;
     const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK>(
         a, tile, &s_buf[cur].rows[0][tid], nullptr, decode_staged<FAM, MODE_STEP>(a, tile, s_buf[cur]), s_obs, [&] {
       if (it > 0) {  // the previous tile's store must have read s_obs
