@@ -33,7 +33,7 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
   const int y = p / RW, x0 = 8 * (p % RW);
   uint64_t r = 0;
   for (int x = x0; x < x0 + 8 && x < W; ++x) {
-    bool wall;
+    bool wall = false;
     if (FAM == FAM_GOTODOOR) wall = false;  // the generator draws the room
     else if (FAM == FAM_KEYCORRIDOR) wall = (x % (Cfg<FAM, H, W>::RS - 1) == 0) || (y % (Cfg<FAM, H, W>::RS - 1) == 0);
     else wall = x == 0 || y == 0 || x == W - 1 || y == H - 1;
