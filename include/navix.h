@@ -118,6 +118,11 @@ NAVIX_API navix_status navix_create_shard(const char* env_id, int64_t num_envs_t
  *        16-byte aligned buffer enables the per-tile TMA bulk store). */
 NAVIX_API navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream);
 
+/* reset(key) with a new key (Code 1 P:264): the handle's seed becomes
+ * `seed` for this and every later level / obstacle draw, then navix_reset.
+ * Equivalent to destroying the handle and creating it with `seed`. */
+NAVIX_API navix_status navix_reset_seed(navix_env* h, uint64_t seed, uint8_t* obs, void* stream);
+
 /* One step of every env with next-step auto-reset (R#18):
  *  actions     (dev) uint8[n]
  *  obs         (dev) uint8[n][7][7][3] (16-byte aligned: bulk-store fast path)

@@ -301,6 +301,12 @@ navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream) {
   return launch(h, MODE_RESET, a, stream);
 }
 
+navix_status navix_reset_seed(navix_env* h, uint64_t seed, uint8_t* obs, void* stream) {
+  if (!h || !obs) return fail(NAVIX_E_INVALID_ARG, "navix_reset_seed: null handle or obs");
+  h->seed = seed;  // the Philox key of every later level / obstacle draw
+  return navix_reset(h, obs, stream);
+}
+
 navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t* obs, float* reward, uint8_t* terminated,
                         uint8_t* truncated, void* stream) {
   if (!h || !actions || !obs || !reward || !terminated || !truncated)

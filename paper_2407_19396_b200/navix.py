@@ -28,7 +28,7 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
-    "navix_set_event_functions", "navix_rollout_random", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_set_event_functions", "navix_rollout_random", "navix_reset_seed", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -75,6 +75,7 @@ def load_library():
         "navix_create": ([ctypes.c_char_p, I64, U64, PP], I32),
         "navix_create_shard": ([ctypes.c_char_p, I64, I64, I64, U64, I32, P, I32, PP], I32),
         "navix_reset": ([P, P, P], I32),
+        "navix_reset_seed": ([P, U64, P, P], I32),
         "navix_step": ([P, P, P, P, P, P, P], I32),
         "navix_observe": ([P, P, P], I32),
         "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
@@ -187,6 +188,14 @@ class NavixEnv:
         obs = self.obs if out is None else out
         self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
         _check(self.lib.navix_reset(self.h, _ptr(obs), _stream(self.device)))
+        return obs
+
+    def reset_seed(self, seed: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """reset(key) with a new key: every later level uses Philox key `seed`."""
+        obs = self.obs if out is None else out
+        self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
+        self.seed = int(seed)
+        _check(self.lib.navix_reset_seed(self.h, self.seed & (2 ** 64 - 1), _ptr(obs), _stream(self.device)))
         return obs
 
     def step(self, actions: torch.Tensor, out=None):

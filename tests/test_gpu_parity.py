@@ -223,3 +223,24 @@ def test_cuda_graph_replay_matches_eager():
 def test_parity_row_f2_more_families(env_id):
     # Empty-Random (random start cell + direction per episode) and DistShift (9x7, lava strips)
     run_parity(env_id, 555, 600, block=555, seed=21)
+
+
+def test_reset_seed_equals_fresh_handle():
+    # reset(key) with a new key: same as a handle created with that seed
+    NavixEnv = navix()
+    n = 777
+    a = NavixEnv("KeyCorridorS3R3-v0", n, seed=1)
+    b = NavixEnv("KeyCorridorS3R3-v0", n, seed=99)
+    o = OracleEnv("KeyCorridorS3R3-v0", n, seed=99)
+    a.reset()
+    a.step(torch.zeros(n, dtype=torch.uint8, device="cuda"))
+    ga = a.reset_seed(99).clone()
+    assert torch.equal(ga, b.reset())
+    np.testing.assert_array_equal(ga.cpu().numpy(), o.reset())
+    acts = random_actions(5, 300, n, 7)
+    for t in range(300):
+        oa = a.step(torch.from_numpy(acts[t]).cuda())[0].clone()
+        ob = b.step(torch.from_numpy(acts[t]).cuda())[0]
+        assert torch.equal(oa, ob), t
+    np.testing.assert_array_equal(a.export_state(), b.export_state())
+    assert torch.equal(a.stats(), b.stats())
