@@ -221,6 +221,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 
   float reward = 0.f;
   bool term = false, trunc = false, grid_dirty = false;
+  int dirty_plane = -1;  // the one row plane an action modified; -1: all (a new level)
   uint32_t st_ep = 0, st_len = 0, st_succ = 0, st_succ_len = 0, st_lava = 0, st_coll = 0, st_trunc = 0,
            st_fail = 0;
 
@@ -392,6 +393,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       carry = pick ? (uint8_t)fc : drop ? CELL_EMPTY : carry;
       if (newf != fc) {
         *fp = (uint8_t)newf;
+        dirty_plane = fy * RW + (fx >> 3);
         grid_dirty = true;
       }
       if (FAM == FAM_KEYCORRIDOR && is_pick && (carry & 15) == K_BALL) success = true;  // R#8
@@ -441,11 +443,17 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   }
 
   // ---- a7a: grid write-back (only when modified), before the lines are reused
+  // (pickup / drop / toggle change one cell: only its 8-byte plane is written,
+  // one 32-byte sector instead of H*RW of them)
   if (MODE != MODE_OBSERVE && grid_dirty && scratch == nullptr) {
     uint64_t* gdst = a.grid + tile0 * H * RW + tid;
+    if (FAM != FAM_DYNOBS && dirty_plane >= 0) {
+      gdst[dirty_plane * TILE] = rows[dirty_plane * TILE];
+    } else {
 #pragma unroll
-    for (int p = 0; p < H * RW; ++p)
-      gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : rows[p * TILE];
+      for (int p = 0; p < H * RW; ++p)
+        gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : rows[p * TILE];
+    }
   }
 
   // ---- a6: observation (obs.cuh); odd directions read world columns

@@ -36,4 +36,6 @@ torch.cuda.synchronize()
 ts = [ev[2 * t].elapsed_time(ev[2 * t + 1]) * 1e3 for t in range(steps)]
 srt = sorted(ts)
 print(f"{env_id} n={n}: median {srt[steps // 2]:.1f} us, mean {sum(ts) / steps:.1f} us, max {srt[-1]:.0f} us")
-print("slowest steps (t, us):", sorted(((round(x), t) for t, x in enumerate(ts)), reverse=True)[:8])
+print("slowest steps (us, t):", sorted(((round(x), t) for t, x in enumerate(ts)), reverse=True)[:8])
+w = max(1, steps // 10)
+print("mean per window of", w, "steps:", [round(sum(ts[i:i + w]) / len(ts[i:i + w]), 1) for i in range(0, steps, w)])
