@@ -107,7 +107,8 @@ NAVIX_API navix_status navix_create(const char* env_id, int64_t num_envs, uint64
  *  state_dev   (dev, nullable) caller-owned buffer of navix_state_bytes(env_id,
  *              num_envs_local) bytes, 256-byte aligned; NULL = the library
  *              cudaMallocs it and frees it in navix_destroy.
- * No kernel runs; call navix_reset before the first step. */
+ * No kernel runs; navix_reset (or navix_state_import) must precede the first
+ * step / rollout / observe (else NAVIX_E_INVALID_ARG). */
 NAVIX_API navix_status navix_create_shard(const char* env_id, int64_t num_envs_total, int64_t env_begin,
                                 int64_t num_envs_local, uint64_t seed, int device, void* state_dev,
                                 int reward_mode, navix_env** out);

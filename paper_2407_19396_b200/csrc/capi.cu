@@ -32,6 +32,7 @@ struct navix_env {
   int device;
   int reward_mode;
   int obs_kind = 0;  // ObsKind (navix_set_observation)
+  bool initialized = false;  // a reset or an import has written the state
   uint32_t reward_events = 7, termination_events = 7;  // navix_set_event_functions (R#42)
   float time_cost = 0.f, action_cost = 0.f;
   uint8_t* state;
@@ -298,7 +299,9 @@ navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream) {
   }
   KernelArgs a = make_args(h);
   a.obs = obs;
-  return launch(h, MODE_RESET, a, stream);
+  const navix_status st = launch(h, MODE_RESET, a, stream);
+  if (st == NAVIX_OK) h->initialized = true;
+  return st;
 }
 
 navix_status navix_reset_seed(navix_env* h, uint64_t seed, uint8_t* obs, void* stream) {
@@ -311,6 +314,7 @@ navix_status navix_step(navix_env* h, const uint8_t* actions, uint8_t* obs, floa
                         uint8_t* truncated, void* stream) {
   if (!h || !actions || !obs || !reward || !terminated || !truncated)
     return fail(NAVIX_E_INVALID_ARG, "navix_step: null argument");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_step: call navix_reset (or navix_state_import) first");
   KernelArgs a = make_args(h);
   a.actions = actions;
   a.obs = obs;
@@ -324,6 +328,7 @@ navix_status navix_rollout(navix_env* h, const uint8_t* actions, int64_t steps, 
                            uint8_t* terminated, uint8_t* truncated, void* stream) {
   if (!h || !actions || !obs || !reward || !terminated || !truncated)
     return fail(NAVIX_E_INVALID_ARG, "navix_rollout: null argument");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_rollout: call navix_reset (or navix_state_import) first");
   if (steps <= 0) return fail(NAVIX_E_INVALID_ARG, "navix_rollout: steps must be positive (got %lld)", (long long)steps);
   KernelArgs a = make_args(h);
   a.actions = actions;
@@ -339,6 +344,7 @@ navix_status navix_rollout_random(navix_env* h, uint64_t action_seed, int64_t t0
                                   float* reward, uint8_t* terminated, uint8_t* truncated, void* stream) {
   if (!h || !obs || !reward || !terminated || !truncated)
     return fail(NAVIX_E_INVALID_ARG, "navix_rollout_random: null argument");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_rollout_random: call navix_reset (or navix_state_import) first");
   if (steps <= 0 || t0 < 0)
     return fail(NAVIX_E_INVALID_ARG, "navix_rollout_random: steps must be positive and t0 >= 0");
   KernelArgs a = make_args(h);
@@ -382,6 +388,7 @@ navix_status navix_set_observation(navix_env* h, int kind) {
 
 navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream) {
   if (!h || !out) return fail(NAVIX_E_INVALID_ARG, "navix_observe_full: null argument");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_observe_full: call navix_reset (or navix_state_import) first");
   KernelArgs a = make_args(h);
   a.obs = out;
   return launch(h, MODE_FULL_OBS, a, stream);
@@ -389,6 +396,7 @@ navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stream) {
 
 navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream) {
   if (!h || !obs) return fail(NAVIX_E_INVALID_ARG, "navix_observe: null argument");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_observe: call navix_reset (or navix_state_import) first");
   KernelArgs a = make_args(h);
   a.obs = obs;
   return launch(h, MODE_OBSERVE, a, stream);
@@ -595,6 +603,7 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
   if (c.family == FAM_DYNOBS &&
       (e = cudaMemcpy(h->state + L.balls_off, balls.data(), balls.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cuda_fail(e, "import H2D balls");
+  h->initialized = true;
   return NAVIX_OK;
 }
 

@@ -244,3 +244,14 @@ def test_reset_seed_equals_fresh_handle():
         assert torch.equal(oa, ob), t
     np.testing.assert_array_equal(a.export_state(), b.export_state())
     assert torch.equal(a.stats(), b.stats())
+
+
+def test_step_before_reset_is_an_error():
+    from paper_2407_19396_b200 import NavixError
+    NavixEnv = navix()
+    g = NavixEnv("DoorKey-8x8-v0", 100)
+    with pytest.raises(NavixError) as e:
+        g.step(torch.zeros(100, dtype=torch.uint8, device="cuda"))
+    assert "navix_reset" in str(e.value)
+    g.reset()
+    g.step(torch.zeros(100, dtype=torch.uint8, device="cuda"))
