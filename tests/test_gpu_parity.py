@@ -255,3 +255,21 @@ def test_step_before_reset_is_an_error():
     assert "navix_reset" in str(e.value)
     g.reset()
     g.step(torch.zeros(100, dtype=torch.uint8, device="cuda"))
+
+
+def test_caller_owned_state_buffer():
+    # navix_create_shard(state_dev = a caller-owned torch buffer of navix_state_bytes)
+    from paper_2407_19396_b200 import state_bytes
+    NavixEnv = navix()
+    n = 1000
+    buf = torch.empty(state_bytes("DoorKey-8x8-v0", n), dtype=torch.uint8, device="cuda")
+    a = NavixEnv("DoorKey-8x8-v0", n, seed=3, state=buf)
+    b = NavixEnv("DoorKey-8x8-v0", n, seed=3)
+    assert torch.equal(a.reset(), b.reset())
+    acts = torch.from_numpy(random_actions(2, 50, n, 7)).cuda()
+    for t in range(50):
+        oa = a.step(acts[t])[0].clone()
+        assert torch.equal(oa, b.step(acts[t])[0]), t
+    np.testing.assert_array_equal(a.export_state(), b.export_state())
+    a.close()
+    assert buf.numel() == state_bytes("DoorKey-8x8-v0", n)  # still owned (not freed) by the caller
