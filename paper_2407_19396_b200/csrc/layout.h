@@ -9,7 +9,7 @@
 //   episode u32 [n_pad]               episode counter (counter word c1, R#20)
 //   balls   u64 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b (<= 8)
 //   stats   u64 [NSLOT][8]            striped int64 episode statistics
-//   sched   u32 [2]                   persistent step kernel tile scheduler
+//   sched   u32 [8 + 4 n_tiles]       persistent step kernel tile scheduler (+ reset-first tile lists)
 // n_pad = num_envs rounded up to TILE.  The struct-of-arrays "row plane"
 // layout makes every warp load of a grid row one contiguous 256-byte segment
 // and lets the kernel fetch a whole world row with one 64-bit load.
@@ -96,8 +96,11 @@ inline StateLayout make_layout(const EnvConfig& c, int64_t n) {
   off = align_up(off + (c.family == FAM_DYNOBS ? (size_t)L.n_pad * 8 : 0), 256);
   L.stats_off = off;
   off = align_up(off + (size_t)NSLOT * 8 * 8, 256);
+  // scheduler: 8 words ([0] ticket, [1] CTAs done, [2] step epoch, [3..4]
+  // list counts by epoch parity), then by epoch parity: per tile the epoch
+  // stamp of "has envs to reset at that step", and the list of those tiles
   L.sched_off = off;
-  off = align_up(off + 2 * sizeof(unsigned int), 256);
+  off = align_up(off + (8 + 4 * (size_t)L.n_tiles) * sizeof(unsigned int), 256);
   L.total = off;
   return L;
 }

@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   auto& s_mbar = S.mbar;
   auto& s_tile = S.tile;
   const int64_t n_tiles = (a.n + TILE - 1) / TILE;
-  unsigned int* const sched = a.sched;          // [0] next tile, [1] CTAs done
+  unsigned int* const sched = a.sched;          // [0] ticket, [1] CTAs done, [2] epoch, [3..4] list counts
+  unsigned int* const marks = sched + 8;        // [2][n_tiles] epoch stamps, then [2][n_tiles] lists
   const int tid = threadIdx.x;
   // fetch the next tile index into s_tile[k] and start its loads on s_mbar[k];
   // with no tile left only arrive (the phase completes), so waiting on
@@ -638,11 +639,38 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     mbar_init(smem_u32(&s_mbar[1]), 1);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Tiles with envs that auto-reset this step (marked by the previous step)
+  // go first: their level generation (a long serial chain for KeyCorridor)
+  // then overlaps the other tiles instead of trailing the step.  Ticket t <
+  // L takes the t-th listed tile, later tickets the tiles in index order,
+  // skipping listed ones.  Epoch stamps make the marks self-clearing.
+  // (stamps and lists are double-buffered by epoch parity: this step reads
+  // the previous step's, and writes the next step's, so a stamp never
+  // changes while it is read)
+  // Only KeyCorridor uses it: its resets are rare but each is a long serial
+  // level generation; families that reset often gain nothing and would pay
+  // the stamp reads and list atomics.
+  constexpr bool RESET_FIRST = FAM == FAM_KEYCORRIDOR;
+  const uint32_t epoch = RESET_FIRST ? sched[2] : 0u;
+  const uint32_t L = (stride_only || !RESET_FIRST) ? 0u : sched[3 + (epoch & 1u)];
+  const unsigned int* mark_cur = marks + (epoch & 1u) * n_tiles;
+  unsigned int* const mark_next = marks + ((epoch + 1u) & 1u) * n_tiles;
+  const unsigned int* list_cur = marks + 2 * n_tiles + (epoch & 1u) * n_tiles;
+  unsigned int* const list_next = marks + 2 * n_tiles + ((epoch + 1u) & 1u) * n_tiles;
+  auto ticket_tile = [&](uint32_t t) -> int64_t {  // thread 0
+    if (stride_only || !RESET_FIRST) return (int64_t)t;
+    for (;;) {
+      if (t < L) return (int64_t)list_cur[t];
+      const int64_t tile = (int64_t)(t - L);
+      if (tile >= n_tiles || mark_cur[tile] != epoch + 1u) return tile;
+      t = atomicAdd(&sched[0], 1u) + 2u * gridDim.x;  // listed: already someone's
+    }
+  };
   if (tid == 0) {
-    // the first two tiles are static (b, b + grid): no burst of contended
+    // the first two tickets are static (b, b + grid): no burst of contended
     // atomics on the scheduler word when every CTA starts at once
-    publish(0, (int64_t)blockIdx.x);
-    publish(1, (int64_t)blockIdx.x + gridDim.x);
+    publish(0, ticket_tile(blockIdx.x));
+    publish(1, ticket_tile(blockIdx.x + gridDim.x));
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -663,8 +691,12 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // all records in s_obs; input buffer cur no longer read
     store_obs<OBSK>(a, tile, s_obs, tid, TILE, tid == 0);
-    if (tid == 0) publish(cur, next);  // tile-after-next into the released buffer
+    if (tid == 0) publish(cur, ticket_tile(next));  // tile-after-next into the released buffer
     tile_store<FAM, MODE_STEP>(a, tile, r);
+    // envs that ended reset at the next step: list their tile for it (once)
+    if (RESET_FIRST && __any_sync(0xffffffffu, r.valid && (r.term || r.trunc)) && (tid & 31) == 0 &&
+        atomicExch(&mark_next[tile], epoch + 2u) != epoch + 2u)
+      list_next[atomicAdd(&sched[3 + ((epoch + 1u) & 1u)], 1u)] = (unsigned int)tile;
   }
   if (tid == 0) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -672,6 +704,10 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the scheduler
       atomicExch(&sched[0], 0u);
       atomicExch(&sched[1], 0u);
+      if (RESET_FIRST) {
+        atomicExch(&sched[3 + (epoch & 1u)], 0u);  // this step's list is consumed
+        atomicExch(&sched[2], epoch + 1u);
+      }
     }
   }
 }
