@@ -213,16 +213,10 @@ __device__ __forceinline__ void view_columns_narrow(const uint64_t* lines, int a
 }
 
 // The same for grids wider than 8 (RW >= 2 u64 planes per row, row f2): row
-// y is clamped into the grid and the window is read from the row with 8 zero
-// bytes prepended (virtual word w < 2 is 0), so every load stays inside this
-// env's H x RW planes; out-of-grid positions read arbitrary bytes (R#12).
-template <int RW, int H>
-__device__ __forceinline__ uint32_t row_word_v(const uint64_t* rows, int y, int w) {
-  const int yc = y < 0 ? 0 : y >= H ? H - 1 : y;
-  const int wc = w < 2 ? 2 : w > 2 * RW + 1 ? 2 * RW + 1 : w;
-  const uint32_t v = reinterpret_cast<const uint32_t*>(rows + (yc * RW + ((wc - 2) >> 1)) * TILE)[wc & 1];
-  return w < 2 ? 0u : v;
-}
+// indices are clamped into the grid and word indices left of a row to word
+// 0, so every load stays inside this env's planes (or, past the last row's
+// last plane, in the SMEM that follows them); out-of-grid positions read
+// arbitrary bytes (R#12).
 template <int RW, int H>
 __device__ __forceinline__ void view_columns_big(const uint64_t* rows, int ax, int ay, int dir, uint32_t (&clo)[7],
                                                  uint32_t (&chi)[7]) {
@@ -230,26 +224,40 @@ __device__ __forceinline__ void view_columns_big(const uint64_t* rows, int ax, i
   const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
   const int s = dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6;  // first position of the window
   const bool rev = dir <= 1;
+  const uint8_t* rb = reinterpret_cast<const uint8_t*>(rows);  // plane p of this env at rb + p * TILE * 8
+  constexpr int ROW_BYTES = RW * TILE * 8, PLANE_BYTES = TILE * 8;
+  auto clamp_y = [](int y) { return y < 0 ? 0 : y > H - 1 ? H - 1 : y; };
   if ((dir & 1) == 0) {
-    const int sv = s + 8, q = sv >> 2, r = 8 * (sv & 3);  // virtual byte offset (>= 2 for ax >= 0)
+    // the 7-byte window of a row from its 32-bit words q-2 .. q (virtual byte
+    // offset s + 8 >= 2, so word indices are those of the row shifted by 2);
+    // words left of the row only hold out-of-grid bytes: read word 0 instead
+    const int sv = s + 8, q = sv >> 2, r = 8 * (sv & 3);
+    auto woff = [](int k) { return (k >> 1) * PLANE_BYTES + (k & 1) * 4; };
+    const int o0 = woff(q - 2 < 0 ? 0 : q - 2), o1 = woff(q - 1 < 0 ? 0 : q - 1), o2 = woff(q);
 #pragma unroll
     for (int vi = 0; vi < 7; ++vi) {
-      const int y = base + sgn * vi;
-      const uint32_t w0 = row_word_v<RW, H>(rows, y, q), w1 = row_word_v<RW, H>(rows, y, q + 1),
-                     w2 = row_word_v<RW, H>(rows, y, q + 2);
+      const uint8_t* rp = rb + clamp_y(base + sgn * vi) * ROW_BYTES;
+      const uint32_t w0 = *reinterpret_cast<const uint32_t*>(rp + o0);
+      const uint32_t w1 = *reinterpret_cast<const uint32_t*>(rp + o1);
+      const uint32_t w2 = *reinterpret_cast<const uint32_t*>(rp + o2);
       const uint32_t f_lo = __funnelshift_r(w0, w1, r), f_hi = __funnelshift_r(w1, w2, r);
       clo[vi] = rev ? prmt(f_lo, f_hi, 0x3456u) : f_lo;
       chi[vi] = rev ? prmt(f_lo, f_hi, 0x0012u) : f_hi;
     }
   } else {
+    // byte x of rows s .. s+6: the clamped row offsets are shared by the 7 columns
+    int roff[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) roff[k] = clamp_y(s + k) * ROW_BYTES;
 #pragma unroll
     for (int vi = 0; vi < 7; ++vi) {
       int x = base + sgn * vi;
       x = x < 0 ? 0 : x > 8 * RW - 1 ? 8 * RW - 1 : x;
+      const uint8_t* cp = rb + (x >> 3) * PLANE_BYTES + ((x >> 2) & 1) * 4;
       const uint32_t xb = (uint32_t)(x & 3), pair = ((4u + xb) << 4) | xb;
       uint32_t w[7];
 #pragma unroll
-      for (int k = 0; k < 7; ++k) w[k] = row_word_v<RW, H>(rows, s + k, (x >> 2) + 2);  // rows s .. s+6, byte x
+      for (int k = 0; k < 7; ++k) w[k] = *reinterpret_cast<const uint32_t*>(cp + roff[k]);
       const uint32_t p01 = prmt(w[0], w[1], pair), p23 = prmt(w[2], w[3], pair);
       const uint32_t p45 = prmt(w[4], w[5], pair), p6 = prmt(w[6], w[6], pair);
       const uint32_t f_lo = prmt(p01, p23, 0x5410u), f_hi = prmt(p45, p6, 0x5410u);  // cells y = s .. s+6
