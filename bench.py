@@ -212,12 +212,15 @@ def run_navix(args, rank, world, local_rank):
     from paper_2407_19396_b200.distributed import (all_reduce_stats, init_process_group, max_over_ranks,
                                                    mean_legacy_return, shard_for)
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank
+    if args.backend == "gloo":  # functional test of the multi-rank path on fewer GPUs (timings meaningless)
+        gpu = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        init_process_group("nccl", dev)
+        init_process_group(args.backend, dev)
     n_total = args.envs_per_gpu * world
     sh = shard_for(n_total, rank, world)
     begin, end, n = sh.begin, sh.end, sh.n
@@ -257,7 +260,7 @@ def run_navix(args, rank, world, local_rank):
     barrier()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(gpu)
     barrier()
     with clk:  # background sampler thread (every 5 ms) for the whole timed region
         ev0.record(s)
@@ -437,6 +440,8 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional tests only)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

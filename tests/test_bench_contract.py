@@ -47,3 +47,37 @@ def test_navix_arm_line():
     assert d["gpu_launches"] == 5
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["rollout"]["value"] > 0 and d["categorical"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_navix_arm_multirank_path_gloo():
+    # the torchrun path (2 ranks, barriers, max over ranks, stats all-reduce,
+    # one line from rank 0) on whatever GPUs exist; gloo so that two ranks may
+    # share one GPU — a functional check, the timings are meaningless
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29731", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "4", "--warmup", "3", "--envs-per-gpu", "4096", "--rollout-steps", "2",
+           "--categorical-steps", "2", "--e2e-steps", "1", "--backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_envs"] == 8192 and d["value"] > 0
+    assert d["cpu_baseline"] is None  # rank 0 at N = 1 only
+    st = d["episode_stats"]
+    assert st["episodes"] >= 0 and st["gen_failures"] == 0
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    # N > 1: rank 0 alone times the oracle and prints; the other ranks exit 0 without work
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29733", os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "3", "--warmup", "3", "--envs-per-gpu", "256",
+           "--ref-budget-s", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
