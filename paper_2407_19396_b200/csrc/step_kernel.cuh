@@ -2,25 +2,27 @@
 // instantiated per family group in inst_*.cu, dispatched in dispatch.cu).
 //
 // One thread owns one environment; one CTA owns a tile of TILE = 128 envs.
-// Per env and step (DESIGN.md §5):
-//   a1 stage      coalesced 64-bit loads of the H grid row planes + agent record
-//                 into SMEM row lines (struct-of-arrays, layout.h)
+// Per env and step (DESIGN.md §5-§6):
+//   a1 stage      TMA bulk copies (cp.async.bulk + mbarrier) of the tile's grid
+//                 row planes, agent records and actions into SMEM; the
+//                 persistent kernel prefetches the next tile while it computes
 //   a2 autoreset  if the previous step ended: episode += 1, Philox level
 //                 generation into the SMEM rows (levelgen.cuh), first obs
 //   a3 transition Dynamic-Obstacles balls (Table 3, App. A)
-//   a4 intervene  left/right/forward/pickup/drop/toggle/done
+//   a4 intervene  left/right/forward/pickup/drop/toggle/done,
+//                 branch-free
 //   a5 reward     Eq. (1) P:216 / P:223 (R#1-R#3), events -> terminated,
-//                 step_count >= T -> truncated (R#17)
-//   a6 observe    symbolic_first_person (Table 5): the 7 view columns
-//                 are 7 world lines (rows or columns, read from SMEM row /
-//                 column copies) shifted and byte-reversed; MiniGrid's
-//                 process_vis as 7-bit row closures computed with one
-//                 integer add each (carry = propagation); SWAR encode of 4
-//                 cells per 32-bit word; interleave (type, colour, state) with
-//                 byte permutes; the 147-byte record assembled in registers
-//   a7 store      obs staged in SMEM, written by ONE cp.async.bulk (TMA bulk
-//                 copy) per tile; reward/flags/agent records coalesced;
-//                 grid rows written back only when modified; episode
+//                 step_count >= T -> truncated (R#17); Table 6/7 selection and
+//                 costs (R#31, R#42)
+//   a6 observe    symbolic_first_person (Table 5) or its categorical
+//                 form (R#41): the 7 view columns are 7 world lines shifted
+//                 and byte-reversed; MiniGrid's process_vis as 7-bit row
+//                 closures computed with one integer add each (carry =
+//                 propagation); SWAR encode of 4 cells per 32-bit word; the
+//                 record assembled in registers at its final byte alignment
+//   a7 store      obs staged in SMEM, written by ONE cp.async.bulk per tile;
+//                 reward/flags/agent records coalesced; a modified grid plane
+//                 written back only when an action changed it; episode
 //                 statistics warp-reduced into striped int64 counters.
 #pragma once
 #include <cstdint>
