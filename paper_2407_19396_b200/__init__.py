@@ -6,6 +6,8 @@ The hot path is ``libnavix.so`` (sm_100a CUDA, C ABI in ``include/navix.h``);
 from .navix import (  # noqa: F401
     EXPORTED_SYMBOLS,
     LIB_PATH,
+    OBS_CATEGORICAL,
+    OBS_SYMBOLIC,
     REWARD_MINIGRID,
     REWARD_NAVIX,
     STATS_FIELDS,
