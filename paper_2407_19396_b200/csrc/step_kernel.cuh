@@ -525,7 +525,34 @@ __device__ __forceinline__ void store_obs(const KernelArgs& a, int64_t tile, con
 
 // a7: per-env global stores and the episode statistics (WRITE_STATE = 0 in a
 // rollout, whose state stays on chip until its last step).
-template <int FAM, int MODE, bool WRITE_STATE = true>
+// Episode statistics of the envs a thread stepped, summed in registers over
+// the tiles of a persistent / rollout CTA and flushed once (warp reduce ->
+// striped int64 atomics) instead of once per tile.
+struct StatsAcc {
+  uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __device__ __forceinline__ void add(const EnvResult& r) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += r.st[k];
+  }
+  __device__ __forceinline__ void flush(const KernelArgs& a) const {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) any |= v[k];
+    if (!__any_sync(0xffffffffu, any != 0)) return;
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = __reduce_add_sync(0xffffffffu, v[k]);
+    if (lane == 0) {
+      unsigned long long* st = a.stats + (size_t)((blockIdx.x * (TILE / 32) + warp) % NSLOT) * 8;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (w[k]) atomicAdd(st + k, (unsigned long long)w[k]);
+    }
+  }
+};
+
+template <int FAM, int MODE, bool WRITE_STATE = true, bool STATS = true>
 __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, const EnvResult& r) {
   if (MODE == MODE_OBSERVE) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -543,6 +570,7 @@ __device__ __forceinline__ void tile_store(const KernelArgs& a, int64_t tile, co
     }
   }
   // episode statistics (info i_{t+1}): warp reduce -> striped atomics
+  if (!STATS) return;  // accumulated by the caller (StatsAcc)
   const unsigned any = __any_sync(0xffffffffu, (r.st[0] | r.st[7]) != 0);
   if (any) {
     uint32_t v[8];
@@ -675,6 +703,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     publish(1, ticket_tile(blockIdx.x + gridDim.x));
   }
   __syncthreads();
+  StatsAcc acc;
   for (int it = 0;; ++it) {
     const int cur = it & 1;
     mbar_wait(smem_u32(&s_mbar[cur]), (uint32_t)(it >> 1) & 1u);
@@ -694,12 +723,14 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
     __syncthreads();  // all records in s_obs; input buffer cur no longer read
     store_obs<OBSK>(a, tile, s_obs, tid, TILE, tid == 0);
     if (tid == 0) publish(cur, ticket_tile(next));  // tile-after-next into the released buffer
-    tile_store<FAM, MODE_STEP>(a, tile, r);
+    tile_store<FAM, MODE_STEP, true, false>(a, tile, r);
+    acc.add(r);
     // envs that ended reset at the next step: list their tile for it (once)
     if (RESET_FIRST && __any_sync(0xffffffffu, r.valid && (r.term || r.trunc)) && (tid & 31) == 0 &&
         atomicExch(&mark_next[tile], epoch + 2u) != epoch + 2u)
       list_next[atomicAdd(&sched[3 + ((epoch + 1u) & 1u)], 1u)] = (unsigned int)tile;
   }
+  acc.flush(a);
   if (tid == 0) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __threadfence();
@@ -739,6 +770,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   mbar_wait(mbar, 0);
   EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
   bool dirty = false;
+  StatsAcc acc;
   // actions from actions[t][n], or drawn in-kernel from the random-policy
   // stream (the one navix_sample_actions writes: bit-identical results)
   const bool draw = a.actions == nullptr;
@@ -768,7 +800,8 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     store_obs<OBSK>(as, tile, s_obs, tid, TILE, tid == 0);
-    tile_store<FAM, MODE_STEP, false>(as, tile, r);
+    tile_store<FAM, MODE_STEP, false, false>(as, tile, r);
+    acc.add(r);
     in.rec = r.nrec;
     in.episode = r.episode;
     in.balls = r.balls;
@@ -785,6 +818,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     for (int p = 0; p < H * C::RW; ++p)
       gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : s_buf.rows[p][tid];
   }
+  acc.flush(a);
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
