@@ -24,7 +24,8 @@
 //
 // Agent record (u64, little endian bytes): 0 x, 1 y, 2 dir, 3 carry (cell
 // byte of the carried object, 0x01 = nothing), 4-5 step_count, 6 flags
-// (bit 0 prev_done), 7 GoToDoor target door (x << 4) | y (else unused).
+// (bit 0 prev_done; bit 1 Dynamic-Obstacles: the HBM grid holds the static
+// template), 7 GoToDoor target door (x << 4) | y (else unused).
 #pragma once
 #include <cstdint>
 

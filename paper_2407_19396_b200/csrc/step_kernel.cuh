@@ -219,6 +219,10 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   uint8_t carry = (uint8_t)(rec >> 24);
   uint32_t sc = (uint32_t)((rec >> 32) & 0xFFFF);
   bool prev_done = (rec >> 48) & 1;
+  // Dynamic-Obstacles: agent-record flag bit 1 = "this env's HBM grid already
+  // holds the static template" (balls live outside it), so a reset need not
+  // write the template back again
+  bool grid_tmpl = FAM == FAM_DYNOBS && ((rec >> 49) & 1);
   uint32_t target = FAM == FAM_GOTODOOR ? (uint32_t)(rec >> 56) : 0u;  // GoToDoor target door
 
   float reward = 0.f;
@@ -268,7 +272,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       carry = CELL_EMPTY;
       sc = 0;
       prev_done = false;
-      grid_dirty = true;
+      grid_dirty = !grid_tmpl;
+      grid_tmpl = FAM == FAM_DYNOBS;
     }
   } else if (regen) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
@@ -284,7 +289,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     carry = CELL_EMPTY;
     sc = 0;
     prev_done = false;
-    grid_dirty = true;
+    grid_dirty = !grid_tmpl;
+    grid_tmpl = FAM == FAM_DYNOBS;
   }
   if (!regen) {
     if (FAM == FAM_DYNOBS) {
@@ -492,7 +498,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.trunc = trunc;
   r.dirty = grid_dirty;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)target << 56);
+           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) |
+           ((uint64_t)target << 56);
   r.episode = episode;
   r.balls = balls;
   const uint32_t vv = valid ? 1u : 0u;
