@@ -164,8 +164,19 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     // distinct colours (one draw over the unused ones, R#37), agent, target
     const int w = 5 + (int)ds.next_bounded((uint32_t)(W - 4));
     const int h = 5 + (int)ds.next_bounded((uint32_t)(H - 4));
-    for (int x = 0; x < w; ++x) { g.set(x, 0, CELL_WALL); g.set(x, h - 1, CELL_WALL); }
-    for (int y = 1; y < h - 1; ++y) { g.set(0, y, CELL_WALL); g.set(w - 1, y, CELL_WALL); }
+    // the wall rectangle as whole 8-byte row planes (the room fits in W <= 8)
+    static_assert(C::RW == 1, "GoToDoor kernels are instantiated for widths <= 8");
+    {
+      const uint64_t in_room = w >= 8 ? ~0ull : (1ull << (8 * w)) - 1;  // bytes x < w
+      const uint64_t empty = 0x0101010101010101ull * CELL_EMPTY;
+      const uint64_t walls = 0x0101010101010101ull * CELL_WALL;
+      const uint64_t side = (0xFFull | (0xFFull << (8 * (w - 1))));  // bytes 0 and w-1
+      const uint64_t full = (walls & in_room) | (empty & ~in_room);
+      const uint64_t mid = (walls & side) | (empty & ~side);
+      constexpr uint64_t in_grid = W >= 8 ? ~0ull : (1ull << (8 * W)) - 1;  // cells x >= W stay 0
+#pragma unroll
+      for (int y = 0; y < H; ++y) g.rows[y * TILE] = ((y == 0 || y == h - 1) ? full : y < h ? mid : empty) & in_grid;
+    }
     const int d0 = 2 + (int)ds.next_bounded((uint32_t)(w - 4));
     const int d1 = 2 + (int)ds.next_bounded((uint32_t)(w - 4));
     const int d2 = 2 + (int)ds.next_bounded((uint32_t)(h - 4));
