@@ -73,6 +73,14 @@ def test_argument_validation_before_any_cuda_call():
     assert state_bytes("DoorKey-8x8-v0", 0) == 0
     assert state_bytes("DoorKey-8x8-v0", 1 << 20) >= (1 << 20) * (64 + 8 + 4)
     assert state_bytes("Foo", 10) == 0
+    assert lib.navix_create_shard(b"DoorKey-8x8-v0", 1 << 33, 0, 10, 0, 0, None, 0, ctypes.byref(h)) == 2
+    assert b"2^32" in lib.navix_last_error()
+    assert lib.navix_create_shard(None, 10, 0, 10, 0, 0, None, 0, ctypes.byref(h)) == 1
+    assert lib.navix_set_observation(None, 1) == 2
+    assert lib.navix_set_event_functions(None, 7, 7) == 2
+    assert lib.navix_set_reward_costs(None, 0.0, 0.0) == 2
+    assert lib.navix_rollout_random(None, 1, 0, 4, None, None, None, None, None) == 2
+    assert lib.navix_reset_seed(None, 1, None, None) == 2
 
 
 def test_shard_ranges_partition():
