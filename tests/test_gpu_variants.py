@@ -88,3 +88,15 @@ def test_event_functions_parity(env_id, mode, rev, tev):
         assert np.array_equal(go.cpu().numpy(), oo), t
     np.testing.assert_array_equal(g.stats().cpu().numpy(), o.stats())
     np.testing.assert_array_equal(g.export_state(), o.export())
+
+
+def test_setter_validation():
+    from paper_2407_19396_b200 import NavixEnv, NavixError
+    g = NavixEnv("DoorKey-8x8-v0", 10)
+    with pytest.raises(NavixError):
+        g.set_event_functions(8, 7)
+    with pytest.raises(NavixError):
+        g.set_reward_costs(-1.0, 0.0)
+    assert g.lib.navix_set_observation(g.h, 2) == 2
+    with pytest.raises(ValueError):
+        NavixEnv("DoorKey-8x8-v0", 10, observation="rgb")
