@@ -81,6 +81,8 @@ def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5)
         times.append(e0.elapsed_time(e1) / 1e3 / (reps * ring))
     t = float(np.percentile(times, 50))
     B = algorithmic_bytes(env.spec)
+    s_ = env.spec
+    Bp = B - s_.height * s_.width + s_.height * 8 * ((s_.width + 7) // 8)
     peak, _ = measured_peaks()
     st = env.stats().cpu().tolist()
     env.close()
@@ -88,6 +90,8 @@ def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5)
     return {"env": env_id, "n": n, "us_per_step": t * 1e6, "env_steps_per_s": n / t,
             "env_steps_per_s_p5_p50_p95": [float(np.percentile(rates, q)) for q in (5, 50, 95)], "runs": runs,
             "GBps": B * n / t / 1e9, "frac_of_measured_hbm": B * n / t / 1e9 / peak, "bytes_per_env_step": B,
+            # the layout's bytes: grid rows padded to 8-byte planes (layout.h)
+            "padded_bytes_per_env_step": Bp, "frac_of_measured_hbm_padded": Bp * n / t / 1e9 / peak,
             "episodes": st[0]}
 
 
@@ -144,8 +148,10 @@ def main():
             else:
                 r = time_point(env_id, n, a.steps, runs=a.runs)
             rows.append(r)
+            pad = r.get("frac_of_measured_hbm_padded")
             print(f"{env_id:28s} N={n:>8d}  {r['us_per_step']:9.2f} us/step  {r['env_steps_per_s'] / 1e9:8.3f} G/s  "
-                  f"{r['GBps']:7.0f} GB/s  {100 * r['frac_of_measured_hbm']:5.1f}%", flush=True)
+                  f"{r['GBps']:7.0f} GB/s  {100 * r['frac_of_measured_hbm']:5.1f}%"
+                  + (f"  (padded rows {100 * pad:5.1f}%)" if pad is not None else ""), flush=True)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump({"gpu": torch.cuda.get_device_name(), "steps": a.steps, "rows": rows}, open(a.out, "w"), indent=1)
 
