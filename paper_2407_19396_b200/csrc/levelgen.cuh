@@ -112,6 +112,9 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
                                               uint32_t klo, uint32_t khi, int gparam) {
   using C = Cfg<FAM, H, W>;
   GenOut o{1, 1, 0, 0u, 0u, 0u};
+  // the rows are this env's SMEM planes: tell the out-of-line generator so its
+  // stores are STS, not generic stores resolved at run time
+  __builtin_assume(__isShared(g.rows));
 #pragma unroll
   for (int p = 0; p < H * C::RW; ++p) g.rows[p * TILE] = template_plane<FAM, H, W>(p);
   DrawStream ds(genv, episode, 0u, klo, khi);
