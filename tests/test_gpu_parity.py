@@ -273,3 +273,37 @@ def test_caller_owned_state_buffer():
     np.testing.assert_array_equal(a.export_state(), b.export_state())
     a.close()
     assert buf.numel() == state_bytes("DoorKey-8x8-v0", n)  # still owned (not freed) by the caller
+
+
+@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "GoToDoor-8x8-v0"])
+def test_parity_dynamic_scheduler_sampled(env_id):
+    # > 4 tiles per CTA: the atomic tile scheduler (and, for KeyCorridor, the
+    # reset-first tile lists) at full scale, 300 steps (KeyCorridor truncates
+    # everyone at 270), sampled blocks against the oracle
+    run_parity(env_id, (1 << 20) + 77, 300, block=96, export_every=100, seed=2)
+
+
+@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "DoorKey-8x8-v0"])
+def test_cuda_graph_replay_dynamic_scheduler(env_id):
+    # graph replays of the persistent kernel in its dynamic-scheduler regime
+    # (epoch-stamped reset-first lists for KeyCorridor) equal eager launches
+    NavixEnv = navix()
+    n, K = (1 << 19) + 1000, 100
+    a = NavixEnv(env_id, n, seed=5)
+    b = NavixEnv(env_id, n, seed=5)
+    a.reset()
+    b.reset()
+    acts = a.sample_actions(1, 0, K)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for t in range(K):
+            a.step(acts[t])
+    for rep in range(3):  # 300 steps: includes KeyCorridor's truncation at 270
+        graph.replay()
+        for t in range(K):
+            b.step(acts[t])
+        torch.cuda.synchronize()
+        assert torch.equal(a.obs, b.obs) and torch.equal(a.reward, b.reward), rep
+    assert np.array_equal(a.export_state(), b.export_state())
+    assert torch.equal(a.stats(), b.stats())
