@@ -275,7 +275,8 @@ def test_caller_owned_state_buffer():
     assert buf.numel() == state_bytes("DoorKey-8x8-v0", n)  # still owned (not freed) by the caller
 
 
-@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "GoToDoor-8x8-v0"])
+@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "GoToDoor-8x8-v0",
+                                    "DistShift1-v0", "SimpleCrossingS11N5-v0", "LavaGapS7-v0"])
 def test_parity_dynamic_scheduler_sampled(env_id):
     # > 4 tiles per CTA: the atomic tile scheduler (and, for KeyCorridor, the
     # reset-first tile lists) at full scale, 300 steps (KeyCorridor truncates
