@@ -5,11 +5,11 @@
  * (§3.2.2, Code 1 P:264 "autoresets when done"), composed
  * of the systems of Table 3: intervention I, transition
  * mu (moving obstacles), observation O = symbolic_first_person
- * (Table 5), reward R (Eq. (1), Table 6) and
+ * (Table 5; or categorical_first_person, R#41), reward R (Eq. (1), Table 6) and
  * termination gamma (Table 7; "all environments terminate when the
  * reward is not 0").  The environments are those of Table 9
  * with MiniGrid's rules.  Readings where the paper is
- * silent are DESIGN.md R#1..R#30.
+ * silent are DESIGN.md R#1..R#42.
  *
  * Conventions
  *  - Pointers marked (dev) are device memory on the handle's device; (host)
@@ -51,7 +51,7 @@ typedef enum {
   NAVIX_E_INVALID_ARG = 2,  /* null pointer, bad count, bad shard range, bad record */
   NAVIX_E_CUDA = 3,         /* a CUDA runtime call or kernel launch failed */
   NAVIX_E_NOMEM = 4,        /* device or pinned allocation failed */
-  NAVIX_E_UNSUPPORTED = 5   /* a Table 9 id this build has no kernel for (grids > 8x8) */
+  NAVIX_E_UNSUPPORTED = 5   /* a parsed id this build has no kernel for (grids > 24x24; none in Table 9) */
 } navix_status;
 
 /* Families of Table 9 with a kernel in this build. */
@@ -79,7 +79,8 @@ typedef struct {
   int32_t view;            /* 7: egocentric view size R (R#14) */
   int32_t n_actions;       /* |A|: 7, or 3 for Dynamic-Obstacles (R#7) */
   int32_t max_steps;       /* T (R#16) */
-  int32_t obs_bytes;       /* 147 = 7*7*3, uint8 [vi][vj][channel] (R#10, R#11) */
+  int32_t obs_bytes;       /* 147 = 7*7*3, uint8 [vi][vj][channel] (R#10, R#11); 49 with
+                            NAVIX_OBS_CATEGORICAL (navix_set_observation) */
   int32_t family;          /* NAVIX_FAMILY_* */
   int32_t n_obstacles;     /* Dynamic-Obstacles balls (R#6), else 0 */
   int32_t export_bytes;    /* canonical per-env record size, see navix_state_export */
@@ -87,8 +88,9 @@ typedef struct {
 
 /* Parse an id such as "Navix-DoorKey-8x8-v0", "MiniGrid-DoorKey-8x8-v0" or
  * "DoorKey-8x8" (Code 1 P:254).  Host only; no CUDA call.
- * Returns NAVIX_E_UNKNOWN_ENV for ids outside Table 9, NAVIX_E_UNSUPPORTED
- * for Table 9 ids whose grid exceeds 8x8 (spec still filled in). */
+ * Returns NAVIX_E_UNKNOWN_ENV for ids outside Table 9 (and MiniGrid's
+ * Dynamic-Obstacles-Random / SimpleCrossing spellings, R#35, R#40).  Every
+ * Table 9 id has a kernel. */
 NAVIX_API navix_status navix_spec_of(const char* env_id, navix_spec* out);
 
 /* Bytes of device state for `num_envs` envs of `env_id` (for a caller-owned
