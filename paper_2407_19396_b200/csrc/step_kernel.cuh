@@ -623,7 +623,9 @@ __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const Kern
   __syncthreads();
   store_obs<OBSK>(a, blockIdx.x, S.obs, threadIdx.x, TILE, threadIdx.x == 0);
   tile_store<FAM, MODE>(a, blockIdx.x, r);
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // exit once the bulk store has READ the staging buffer; its global writes
+  // complete with the grid (the TMA-store epilogue idiom)
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // Persistent step: each CTA pulls tiles from a global atomic scheduler and
@@ -739,7 +741,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   }
   acc.flush(a);
   if (tid == 0) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // SMEM read; writes complete with the grid
     __threadfence();
     if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the scheduler
       atomicExch(&sched[0], 0u);
@@ -826,7 +828,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
       gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : s_buf.rows[p][tid];
   }
   acc.flush(a);
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // f3 (Table 5 `symbolic`): the full-grid encoding of MiniGrid's
