@@ -689,15 +689,18 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   // Only KeyCorridor uses it: its resets are rare but each is a long serial
   // level generation; families that reset often gain nothing and would pay
   // the stamp reads and list atomics.
-  constexpr bool RESET_FIRST = FAM == FAM_KEYCORRIDOR;
+  // (striding, the small-batch mode, has no claim order to change: off there;
+  // the mode is fixed for a handle, so the lists stay consistent)
+  constexpr bool RESET_FIRST_FAM = FAM == FAM_KEYCORRIDOR;
+  const bool RESET_FIRST = RESET_FIRST_FAM && !stride_only;
   const uint32_t epoch = RESET_FIRST ? sched[2] : 0u;
-  const uint32_t L = (stride_only || !RESET_FIRST) ? 0u : sched[3 + (epoch & 1u)];
+  const uint32_t L = RESET_FIRST ? sched[3 + (epoch & 1u)] : 0u;
   const unsigned int* mark_cur = marks + (epoch & 1u) * n_tiles;
   unsigned int* const mark_next = marks + ((epoch + 1u) & 1u) * n_tiles;
   const unsigned int* list_cur = marks + 2 * n_tiles + (epoch & 1u) * n_tiles;
   unsigned int* const list_next = marks + 2 * n_tiles + ((epoch + 1u) & 1u) * n_tiles;
   auto ticket_tile = [&](uint32_t t) -> int64_t {  // thread 0
-    if (stride_only || !RESET_FIRST) return (int64_t)t;
+    if (!RESET_FIRST) return (int64_t)t;
     for (;;) {
       if (t < L) return (int64_t)list_cur[t];
       const int64_t tile = (int64_t)(t - L);
@@ -740,8 +743,10 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
       list_next[atomicAdd(&sched[3 + ((epoch + 1u) & 1u)], 1u)] = (unsigned int)tile;
   }
   acc.flush(a);
-  if (tid == 0) {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // SMEM read; writes complete with the grid
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // SMEM read; writes complete with the grid
+  // Pure striding claims no tickets, so (outside KeyCorridor's epochs) there
+  // is nothing to reset and no exit atomic on the small-batch critical path.
+  if (tid == 0 && (RESET_FIRST || !stride_only)) {
     __threadfence();
     if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the scheduler
       atomicExch(&sched[0], 0u);
