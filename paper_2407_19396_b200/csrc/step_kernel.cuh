@@ -608,6 +608,10 @@ template <int FAM, int H, int W, int MODE, int OBSK>
 __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const KernelArgs a) {
   using C = Cfg<FAM, H, W>;
   auto& S = *reinterpret_cast<OneTileSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
+  if (MODE == MODE_STEP) {  // launched with programmatic dependent launch (see navix_step_persistent)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (MODE != MODE_RESET) {
     const uint32_t mbar = smem_u32(&S.mbar);
     if (threadIdx.x == 0) {
@@ -920,7 +924,17 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   constexpr bool PERSIST = H * C::RW <= 24;
   constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
   if (mode == MODE_STEP && (onetile || !PERSIST)) {
-    navix_kernel<FAM, H, W, MODE_STEP, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)n_tiles);
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = DYN;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, navix_kernel<FAM, H, W, MODE_STEP, OBSK>, a);
   } else if (mode == MODE_STEP) {
     if constexpr (PERSIST) {
       // persistent grid: as many CTAs as fit on the device at once
