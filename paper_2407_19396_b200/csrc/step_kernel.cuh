@@ -237,7 +237,9 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // level generator for a few lanes.  Their resetting envs are queued per CTA
   // instead and generated by the first threads (one warp for up to 32 of
   // them), each into its env's SMEM rows.
-  constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
+  // (measured: the queue pays on the narrow persistent kernel, not on the
+  // 16x16 one-tile kernel, where it costs 8 % at 2^20 and 50 % at 2^16 envs)
+  constexpr bool COMPACT = ((FAM == FAM_DYNOBS && RW == 1) || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   if (COMPACT) {
     __shared__ int s_qn;
     __shared__ int s_q[TILE];
