@@ -17,7 +17,7 @@ import json
 import os
 import platform
 import sys
-import threading
+import subprocess
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -53,88 +53,84 @@ def committed_traffic(env_id: str):
     return d.get(env_id)
 
 
+# Sampler process: NVML SM clock + clock-event reasons every ~1 ms, one line
+# "t_monotonic mhz reasons_mask" per sample, until stdin closes.  A separate
+# process keeps sampling while the main thread sits in a blocking graph launch.
+_SAMPLER = r"""
+import os, select, sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+log = open(sys.argv[2], "w")  # a file, not the pipe: the parent reads it only at the end
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], 0.0005)
+    if r and not os.read(sys.stdin.fileno(), 64):
+        break
+    try:
+        m = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        q = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        log.write("%r %d %d\n" % (time.monotonic(), m, q))
+    except Exception:
+        pass
+log.close()
+"""
+
+_REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80}
+
+
 class ClockSampler:
-    """NVML clocks + throttle reasons sampled in a thread during the timed region."""
+    """SM clocks and throttle reasons sampled by a separate process during the
+    timed region (`start()` early, `mark()` around the region, `summary()`)."""
 
-    def __init__(self, index: int, period_s: float = 0.001):
-        self.samples, self.reasons = [], set()
-        self.period, self.ok = period_s, False
+    def __init__(self, index: int):
+        self.index, self.proc, self.max_mhz = index, None, None
+        self.t0 = self.t1 = None
+
+    def start(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception:  # pragma: no cover - no NVML
-            self.max_mhz = None
-        self._stop = threading.Event()
-
-    def _run(self):
-        nv = self.nv
-        names = {
-            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
-            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
-            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
-            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
-            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
-        }
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit:
-                        self.reasons.add(k)
-            except Exception:
-                pass
-            time.sleep(self.period)
-
-    def sample_once(self):
-        nv = self.nv
-        names = {
-            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
-            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
-            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
-            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
-            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
-        }
-        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-        for k, bit in names.items():
-            if r & bit:
-                self.reasons.add(k)
-
-    def poll_until(self, event):
-        """Sample until `event` (recorded at the end of the timed region) completes."""
-        if not self.ok:
-            return
-        while True:
-            done = event.query()
-            try:
-                self.sample_once()
-            except Exception:
-                return
-            if done:
-                return
-
-    def __enter__(self):
-        if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+            import tempfile
+            fd, self.path = tempfile.mkstemp(prefix="navix_clocks_", suffix=".txt")
+            os.close(fd)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index), self.path],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            first = self.proc.stdout.readline().split()  # blocks until NVML is up
+            self.max_mhz = int(first[1]) if first and first[0] == "max" else None
+        except Exception:  # pragma: no cover - no NVML / sampler
+            self.proc = None
         return self
 
-    def __exit__(self, *a):
-        if self.ok:
-            self._stop.set()
-            self.t.join()
+    def mark_begin(self):
+        self.t0 = time.monotonic()
+
+    def mark_end(self):
+        self.t1 = time.monotonic()
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        s = sorted(self.samples)
-        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(s)}
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            self.proc.communicate(input="", timeout=30)
+            with open(self.path) as f:
+                out = f.read()
+            os.remove(self.path)
+        except Exception:  # pragma: no cover
+            self.proc.kill()
+            out = ""
+        rows = []
+        for line in out.splitlines():
+            f = line.split()
+            if len(f) == 3:
+                rows.append((float(f[0]), int(f[1]), int(f[2])))
+        window = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        if not window and rows:  # region shorter than one sample: the nearest ones
+            window = sorted(rows, key=lambda r: abs(r[0] - (self.t1 or r[0])))[:3]
+        mhz = sorted(r[1] for r in window)
+        reasons = sorted({k for r in window for k, bit in _REASONS.items() if r[2] & bit})
+        return {"sm_mhz": mhz[len(mhz) // 2] if mhz else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(window)}
 
 
 def cpu_info():
@@ -215,6 +211,7 @@ def run_navix(args, rank, world, local_rank):
     gpu = local_rank
     if args.backend == "gloo":  # functional test of the multi-rank path on fewer GPUs (timings meaningless)
         gpu = local_rank % torch.cuda.device_count()
+    clk = ClockSampler(gpu).start()  # up and sampling before the timed region
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
     dist = None
@@ -260,21 +257,18 @@ def run_navix(args, rank, world, local_rank):
     barrier()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(gpu)
     barrier()
-    with clk:  # background sampler thread (every 5 ms) for the whole timed region
-        ev0.record(s)
-        if graphs:
-            for gph in graphs:
-                gph.replay()
-        else:
-            for t in range(args.steps):
-                env.step(acts[t % ring])
-        ev1.record(s)
-        # the launches are queued: also sample clocks / throttle reasons from
-        # this thread while the device is still inside the timed region
-        clk.poll_until(ev1)
-        torch.cuda.synchronize(dev)
+    clk.mark_begin()  # the sampler process covers the whole timed region
+    ev0.record(s)
+    if graphs:
+        for gph in graphs:
+            gph.replay()
+    else:
+        for t in range(args.steps):
+            env.step(acts[t % ring])
+    ev1.record(s)
+    torch.cuda.synchronize(dev)
+    clk.mark_end()
     t_local = ev0.elapsed_time(ev1) / 1e3
     t_max = max_over_ranks(t_local, dev)
     value = n_total * args.steps / t_max
