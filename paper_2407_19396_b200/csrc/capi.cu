@@ -116,7 +116,8 @@ int parse_id(const char* env_id, EnvConfig* c) {
     if (a < 5 || a > 7) return 1;
     *c = EnvConfig{FAM_LAVAGAP, a, a, 4 * a * a, 7, 0, 0, 0};
   } else if (sscanf(id.c_str(), "KeyCorridorS%dR%d%c", &a, &b, &tail) == 2) {
-    if (a < 3 || a > 6 || b < 1 || b > 3) return 1;
+    // the registered configurations (Table 9): S3R1-S3R3, S4R3, S5R3, S6R3
+    if (!((a == 3 && b >= 1 && b <= 3) || (a >= 4 && a <= 6 && b == 3))) return 1;
     *c = EnvConfig{FAM_KEYCORRIDOR, (a - 1) * b + 1, (a - 1) * 3 + 1, 30 * a * a, 7, 0, a, b};
   } else {
     return 1;

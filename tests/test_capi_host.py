@@ -93,3 +93,31 @@ def test_shard_ranges_partition():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(e - b for b, e in rs) - min(e - b for b, e in rs) <= 1
+
+
+def test_every_id_the_library_accepts_the_oracle_parses_identically():
+    # the two independent id parsers: whatever libnavix accepts (one id per
+    # kernel instantiation, many spellings), the oracle parses to the same spec
+    from oracle import spec_of as oracle_spec
+    from paper_2407_19396_b200 import NavixError, spec_of
+    fams = ["Empty-{s}x{s}", "Empty-Random-{s}x{s}", "DoorKey-{s}x{s}", "DoorKey-Random-{s}x{s}",
+            "Dynamic-Obstacles-{s}x{s}", "Dynamic-Obstacles-Random-{s}x{s}", "LavaGapS{s}", "GoToDoor-{s}x{s}",
+            "KeyCorridorS{s}R1", "KeyCorridorS{s}R2", "KeyCorridorS{s}R3", "SimpleCrossingS{s}N1",
+            "SimpleCrossingS{s}N2", "SimpleCrossingS{s}N3", "SimpleCrossingS{s}N5", "Crossings-S{s}N5"]
+    extra = ["FourRooms", "DistShift1", "DistShift2"]
+    accepted = 0
+    for pre in ("", "Navix-", "MiniGrid-"):
+        for suf in ("", "-v0"):
+            ids = [pre + f.format(s=s) + suf for f in fams for s in range(2, 19)] + [pre + e + suf for e in extra]
+            for env_id in ids:
+                try:
+                    s = spec_of(env_id)
+                except NavixError:
+                    continue
+                accepted += 1
+                o = oracle_spec(env_id)
+                assert (o.height, o.width, o.max_steps, o.n_actions, o.family, o.export_bytes, o.n_obstacles) == \
+                    (s.height, s.width, s.max_steps, s.n_actions, s.family, s.export_bytes, s.n_obstacles), env_id
+    # 44 kernel-backed ids (every Table 9 id, plus DoorKey / Dynamic-Obstacles
+    # -Random at every size and both Crossing spellings) x 6 spellings
+    assert accepted == 6 * 44
