@@ -100,3 +100,32 @@ def test_setter_validation():
     assert g.lib.navix_set_observation(g.h, 2) == 2
     with pytest.raises(ValueError):
         NavixEnv("DoorKey-8x8-v0", 10, observation="rgb")
+
+
+def test_every_accepted_id_has_a_kernel():
+    # every id navix_spec_of accepts launches (reset, steps, observe, rollout,
+    # full observation) in both observation kinds
+    from paper_2407_19396_b200 import NavixEnv, NavixError, spec_of
+    fams = ["Empty-{s}x{s}", "Empty-Random-{s}x{s}", "DoorKey-{s}x{s}", "DoorKey-Random-{s}x{s}",
+            "Dynamic-Obstacles-{s}x{s}", "Dynamic-Obstacles-Random-{s}x{s}", "LavaGapS{s}", "GoToDoor-{s}x{s}",
+            "KeyCorridorS{s}R1", "KeyCorridorS{s}R2", "KeyCorridorS{s}R3", "SimpleCrossingS{s}N1",
+            "SimpleCrossingS{s}N2", "SimpleCrossingS{s}N3", "SimpleCrossingS{s}N5"]
+    ids = [f.format(s=s) for f in fams for s in range(2, 19)] + ["FourRooms", "DistShift1", "DistShift2"]
+    n_ok = 0
+    for env_id in ids:
+        try:
+            spec_of(env_id)
+        except NavixError:
+            continue
+        for obs in ("symbolic", "categorical"):
+            g = NavixEnv(env_id, 130, seed=1, observation=obs)
+            g.reset()
+            for t in range(3):
+                g.step(g.sample_actions(2, t, 1)[0])
+            g.rollout_random(3, 3, 2)
+            g.observe()
+            g.observe_full()
+            torch.cuda.synchronize()
+            g.close()
+        n_ok += 1
+    assert n_ok == 43
