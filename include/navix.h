@@ -202,6 +202,12 @@ NAVIX_API navix_status navix_observe_full(navix_env* h, uint8_t* out, void* stre
 /* The current observation of every env without stepping (O: S -> O, Table 3). */
 NAVIX_API navix_status navix_observe(navix_env* h, uint8_t* obs, void* stream);
 
+/* GoToDoor's mission (Table 6 / 7 `on_door_done`: "the colour specified in
+ * the mission"; R#37): out (dev) uint8[n] = MiniGrid colour
+ * index (0 red .. 5 grey) of each env's target door, for the current
+ * episode.  NAVIX_E_INVALID_ARG for other families. */
+NAVIX_API navix_status navix_observe_mission(navix_env* h, uint8_t* out, void* stream);
+
 /* The random policy of the bench (R#20, domain 2):
  * out[t][i] = bounded(word0(Philox(ctr=(env_begin+i, t0+t, 2<<16, 0),
  * key=action_seed)), n_actions).   out (dev) uint8[steps][n]. */

@@ -19,6 +19,8 @@ cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a,
 cudaError_t launch_sample_actions(uint8_t* out, int64_t n, int64_t steps, uint32_t env_begin, uint32_t t0,
                                   uint64_t seed, uint32_t n_actions, cudaStream_t s);
 cudaError_t launch_stats_reduce(const unsigned long long* slots, long long* out8, cudaStream_t s);
+cudaError_t launch_mission(const uint64_t* grid, const uint64_t* agent, int64_t n, int rw, int h, uint8_t* out,
+                           cudaStream_t s);
 }  // namespace navix
 
 using namespace navix;
@@ -445,6 +447,19 @@ navix_status navix_step_host(navix_env* h, const uint8_t* actions, uint8_t* obs,
       (e = cudaMemcpyAsync(truncated, h->h_trunc, n, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return cuda_fail(e, "D2H step outputs");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return NAVIX_OK;
+}
+
+navix_status navix_observe_mission(navix_env* h, uint8_t* out, void* stream) {
+  if (!h || !out) return fail(NAVIX_E_INVALID_ARG, "navix_observe_mission: null argument");
+  if (h->cfg.family != FAM_GOTODOOR)
+    return fail(NAVIX_E_INVALID_ARG, "navix_observe_mission: only GoToDoor has a mission");
+  if (!h->initialized) return fail(NAVIX_E_INVALID_ARG, "navix_observe_mission: call navix_reset first");
+  DeviceGuard dg(h->device);
+  cudaError_t e = launch_mission(reinterpret_cast<const uint64_t*>(h->state + h->layout.grid_off),
+                                 reinterpret_cast<const uint64_t*>(h->state + h->layout.agent_off), h->n,
+                                 row_planes(h->cfg.width), h->cfg.height, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mission launch");
   return NAVIX_OK;
 }
 

@@ -44,6 +44,28 @@ __global__ void stats_reduce_kernel(const unsigned long long* slots, long long* 
   }
 }
 
+// GoToDoor's mission (Table 6 `on_door_done`, "the colour specified in the
+// mission"): the colour of each env's target door, read from the agent
+// record (byte 7 = (x << 4) | y) and the HBM grid.  out[e] in 0..5.
+__global__ void mission_kernel(const uint64_t* grid, const uint64_t* agent, int64_t n, int rw, int h,
+                               uint8_t* out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = e / TILE, slot = tile * TILE + slot_of_env((int)(e % TILE));
+    const uint32_t t = (uint32_t)(agent[slot] >> 56);
+    const int x = (int)(t >> 4), y = (int)(t & 15);
+    const uint64_t plane = grid[(tile * h * rw + y * rw + (x >> 3)) * TILE + (slot - tile * TILE)];
+    out[e] = (uint8_t)((plane >> (8 * (x & 7) + 4)) & 7);
+  }
+}
+
+cudaError_t launch_mission(const uint64_t* grid, const uint64_t* agent, int64_t n, int rw, int h, uint8_t* out,
+                           cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  mission_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(grid, agent, n, rw, h, out);
+  return cudaPeekAtLastError();
+}
+
 cudaError_t launch_env_kernel(const EnvConfig& c, int mode, const KernelArgs& a, int64_t n_tiles, cudaStream_t s) {
   static const GroupLauncher groups[] = {launch_group_empty, launch_group_doorkey, launch_group_dynobs, launch_group_keycorridor, launch_group_lava_crossing_distshift, launch_group_gotodoor_fourrooms};
   const int key = c.family * 10000 + c.height * 100 + c.width;

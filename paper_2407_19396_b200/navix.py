@@ -28,7 +28,7 @@ STATS_FIELDS = ("episodes", "sum_len", "n_success", "sum_success_step",
 EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
-    "navix_set_event_functions", "navix_rollout_random", "navix_reset_seed", "navix_sample_actions", "navix_step_host", "navix_stats",
+    "navix_set_event_functions", "navix_rollout_random", "navix_reset_seed", "navix_observe_mission", "navix_sample_actions", "navix_step_host", "navix_stats",
     "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
 )
 
@@ -81,6 +81,7 @@ def load_library():
         "navix_rollout": ([P, P, I64, P, P, P, P, P], I32),
         "navix_rollout_random": ([P, U64, I64, I64, P, P, P, P, P], I32),
         "navix_observe_full": ([P, P, P], I32),
+        "navix_observe_mission": ([P, P, P], I32),
         "navix_set_reward_costs": ([P, ctypes.c_float, ctypes.c_float], I32),
         "navix_set_observation": ([P, I32], I32),
         "navix_set_event_functions": ([P, ctypes.c_uint32, ctypes.c_uint32], I32),
@@ -265,6 +266,13 @@ class NavixEnv:
         o = torch.empty((self.n, *self.full_shape), dtype=torch.uint8, device=self.device) if out is None else out
         self._check_out(o, (self.n, *self.full_shape), torch.uint8)
         _check(self.lib.navix_observe_full(self.h, _ptr(o), _stream(self.device)))
+        return o
+
+    def observe_mission(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """GoToDoor: uint8[n] colour index of each env's target door (the mission)."""
+        o = torch.empty(self.n, dtype=torch.uint8, device=self.device) if out is None else out
+        self._check_out(o, (self.n,), torch.uint8)
+        _check(self.lib.navix_observe_mission(self.h, _ptr(o), _stream(self.device)))
         return o
 
     def observe(self, out: torch.Tensor | None = None) -> torch.Tensor:

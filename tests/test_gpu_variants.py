@@ -129,3 +129,28 @@ def test_every_accepted_id_has_a_kernel():
             g.close()
         n_ok += 1
     assert n_ok == 43
+
+
+def test_gotodoor_mission_matches_the_oracle_target():
+    # the mission colour = the colour of the oracle's target door (its record's
+    # last two bytes give the target (x, y)), across auto-resets
+    from paper_2407_19396_b200 import NavixEnv, NavixError
+    for S in (5, 6, 8):
+        env_id = f"GoToDoor-{S}x{S}-v0"
+        n = 700
+        g = NavixEnv(env_id, n, seed=7)
+        o = OracleEnv(env_id, n, seed=7)
+        g.reset()
+        o.reset()
+        acts = random_actions(4, 30, n, 7)
+        for t in range(30):
+            g.step(torch.from_numpy(acts[t]).cuda())
+            o.step(acts[t])
+            rec = o.export()
+            tx, ty = rec[:, -2].astype(int), rec[:, -1].astype(int)
+            cells = rec[:, :3 * S * S].reshape(n, S, S, 3)
+            want = cells[np.arange(n), ty, tx, 1]
+            assert np.all(cells[np.arange(n), ty, tx, 0] == 4)  # the target is a door
+            np.testing.assert_array_equal(g.observe_mission().cpu().numpy(), want, err_msg=f"{env_id} t={t}")
+    with pytest.raises(NavixError):
+        NavixEnv("DoorKey-8x8-v0", 10).observe_mission()
