@@ -308,3 +308,27 @@ def test_cuda_graph_replay_dynamic_scheduler(env_id):
         assert torch.equal(a.obs, b.obs) and torch.equal(a.reward, b.reward), rep
     assert np.array_equal(a.export_state(), b.export_state())
     assert torch.equal(a.stats(), b.stats())
+
+
+def test_side_stream_and_graph_on_side_stream():
+    # every call enqueues on torch's current stream: a side stream gives the
+    # same results as the default one
+    NavixEnv = navix()
+    n = 3000
+    a = NavixEnv("LavaGapS7-v0", n, seed=8)
+    b = NavixEnv("LavaGapS7-v0", n, seed=8)
+    acts = torch.from_numpy(random_actions(6, 60, n, 7)).cuda()
+    a.reset()
+    for t in range(60):
+        a.step(acts[t])
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        b.reset()
+        for t in range(60):
+            b.step(acts[t])
+        ob = b.obs.clone()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    assert torch.equal(a.obs, ob)
+    np.testing.assert_array_equal(a.export_state(), b.export_state())
