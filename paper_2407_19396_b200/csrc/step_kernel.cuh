@@ -922,8 +922,10 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
     onetile = v && v[0] == 'o';
   }
   // the persistent kernel double-buffers the tile inputs in SMEM: grids up
-  // to 24 row planes (e.g. 12 rows of 9-16 cells); larger ones run one tile per CTA
-  constexpr bool PERSIST = H * C::RW <= 24;
+  // to 16 row planes (8x8 and below, DistShift's 7 rows of 9); larger ones run
+  // one tile per CTA, whose single buffer keeps more CTAs per SM (measured:
+  // KeyCorridorS4R3 +24 %, SimpleCrossingS9N3 +11 % on the one-tile kernel)
+  constexpr bool PERSIST = H * C::RW <= 16;
   constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
   if (mode == MODE_STEP && (onetile || !PERSIST)) {
     cudaLaunchConfig_t cfg = {};
