@@ -12,6 +12,13 @@ BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_ste
              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches"}
 
 
+def _free_port() -> str:
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return str(sock.getsockname()[1])
+
+
 def _run(args, timeout=600):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
                        timeout=timeout, cwd=ROOT)
@@ -55,7 +62,7 @@ def test_navix_arm_multirank_path_gloo():
     # one line from rank 0) on whatever GPUs exist; gloo so that two ranks may
     # share one GPU — a functional check, the timings are meaningless
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29731", os.path.join(ROOT, "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", _free_port(), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "4", "--warmup", "3", "--envs-per-gpu", "4096", "--rollout-steps", "2",
            "--categorical-steps", "2", "--e2e-steps", "1", "--backend", "gloo"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
@@ -72,7 +79,7 @@ def test_navix_arm_multirank_path_gloo():
 def test_reference_arm_under_torchrun_prints_once():
     # N > 1: rank 0 alone times the oracle and prints; the other ranks exit 0 without work
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29733", os.path.join(ROOT, "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", _free_port(), os.path.join(ROOT, "bench.py"),
            "--impl", "reference", "--gpus", "2", "--steps", "3", "--warmup", "3", "--envs-per-gpu", "256",
            "--ref-budget-s", "2"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
