@@ -22,6 +22,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
+    *os.environ.get("NAVIX_EXTRA_NVCC_FLAGS", "").split(),  # A/B experiments only
 ]
 
 

@@ -107,7 +107,17 @@ __device__ __forceinline__ int select_bits(const uint64_t (&m)[NW], uint32_t k) 
   return -1;
 }
 
-template <int FAM, int H, int W>
+// word t (0..7) of the two consecutive Philox blocks (x0, x1)
+__device__ __forceinline__ uint32_t pick8(const uint4& x0, const uint4& x1, uint32_t t) {
+  const uint4& x = t < 4 ? x0 : x1;
+  const uint32_t u = t & 3;
+  return u == 0 ? x.x : u == 1 ? x.y : u == 2 ? x.z : x.w;
+}
+
+// WARP: the whole warp calls this for ONE env (same arguments in every lane,
+// converged) and KeyCorridor's connect_all runs 32 of its iterations at once
+// (see the loop); every other family and step is computed redundantly.
+template <int FAM, int H, int W, bool WARP = false>
 __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, uint32_t genv, uint32_t episode,
                                               uint32_t klo, uint32_t khi, int gparam) {
   using C = Cfg<FAM, H, W>;
@@ -411,6 +421,53 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       return reach;
     };
     uint32_t reach = closure(1u << ((o.ay / (S - 1)) * NC + o.ax / (S - 1)));
+    if constexpr (WARP) {
+      // The same loop, 32 iterations per round: lane l evaluates iteration
+      // it + l as if iterations it .. it + l - 1 were all skips (3 draws
+      // each, no state change), i.e. from draw p + 3l.  The first lane that
+      // adds a door (or passes the 5000 cap) is the one the sequential loop
+      // reaches; its add is applied and the next round starts after its 4th
+      // draw.  Same draws, same result, ~#doors + #iterations/32 rounds.
+      const uint32_t lane = threadIdx.x & 31;
+      uint32_t p = ds.pos;
+      int it = 0;
+      for (;;) {
+        if (it > 5000) { o.fail += 1; break; }
+        if (reach == all) break;
+        const uint32_t q = p + 3u * lane, b0 = q >> 2, t0 = q & 3;
+        const uint4 x0 = philox4x32_10(make_uint4(genv, episode, 0u, b0), klo, khi);
+        const uint4 x1 = philox4x32_10(make_uint4(genv, episode, 0u, b0 + 1u), klo, khi);
+        const int i = (int)bounded(pick8(x0, x1, t0), NC);
+        const int j = (int)bounded(pick8(x0, x1, t0 + 1), NR);
+        const int k = (int)bounded(pick8(x0, x1, t0 + 2), 4);
+        const uint32_t wc = pick8(x0, x1, t0 + 3);
+        const int r = j * NC + i;
+        const bool has = k == 0 ? i < NC - 1 : k == 1 ? j < NR - 1 : k == 2 ? i > 0 : j > 0;
+        const int nb = k == 0 ? r + 1 : k == 1 ? r + NC : k == 2 ? r - 1 : r - NC;
+        const int lo = r < nb ? r : nb;
+        const bool horiz = (k & 1) == 0;
+        const bool add = has && !(((horiz ? Hl : Vl) >> lo) & 1u) && r != locked_room && nb != locked_room;
+        const uint32_t hit = __ballot_sync(0xffffffffu, add || it + (int)lane > 5000);
+        if (hit == 0) { p += 96u; it += 32; continue; }
+        const int f = __ffs(hit) - 1;
+        it += f;
+        if (it > 5000) { o.fail += 1; break; }
+        const int fr = __shfl_sync(0xffffffffu, r, f), fnb = __shfl_sync(0xffffffffu, nb, f);
+        const int flo = __shfl_sync(0xffffffffu, lo, f);
+        const bool fh = __shfl_sync(0xffffffffu, (int)horiz, f) != 0;
+        const uint8_t col = (uint8_t)bounded(__shfl_sync(0xffffffffu, wc, f), 6);
+        const int li = flo % NC, lj = flo / NC;
+        const int x = fh ? li * (S - 1) + S - 1 : dpx[flo];
+        const int y = fh ? dpy[flo] : lj * (S - 1) + S - 1;
+        g.set(x, y, make_cell(K_DOOR_CLOSED, col));
+        if (fh) Hl |= 1u << flo;
+        else Vl |= 1u << flo;
+        if (((reach >> fr) ^ (reach >> fnb)) & 1u) reach = closure(reach);
+        p += 3u * (uint32_t)f + 4u;
+        it += 1;
+      }
+      return o;
+    }
     for (int it = 0;; ++it) {
       if (it > 5000) { o.fail += 1; break; }
       if (reach == all) break;

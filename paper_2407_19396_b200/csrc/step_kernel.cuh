@@ -33,6 +33,10 @@
 #include "obs.cuh"
 #include "philox.cuh"
 
+#ifndef NAVIX_KC_WARP_MAX
+#define NAVIX_KC_WARP_MAX 4
+#endif
+
 namespace navix {
 
 // ------------------------------------------------------------------ helpers
@@ -240,6 +244,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // (measured: the queue pays on the narrow persistent kernel, not on the
   // 16x16 one-tile kernel, where it costs 8 % at 2^20 and 50 % at 2^16 envs)
   constexpr bool COMPACT = ((FAM == FAM_DYNOBS && RW == 1) || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
+  constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
+  constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
   if (COMPACT) {
     __shared__ int s_qn;
     __shared__ int s_q[TILE];
@@ -277,22 +283,47 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       grid_dirty = !grid_tmpl;
       grid_tmpl = FAM == FAM_DYNOBS;
     }
-  } else if (regen) {
+  } else if (KC_WARP || regen) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
-    if (MODE == MODE_STEP) {
+    if (MODE == MODE_STEP && regen) {
       if (!in.episode_known) episode = a.episode[slot];
       episode += 1;
     }
-    const GenOut o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi, a.gen_param);
-    ax = o.ax; ay = o.ay; dir = o.dir;
-    target = o.target;
-    balls = o.balls;
-    st_fail = o.fail;
-    carry = CELL_EMPTY;
-    sc = 0;
-    prev_done = false;
-    grid_dirty = !grid_tmpl;
-    grid_tmpl = FAM == FAM_DYNOBS;
+    GenOut o;
+    if constexpr (KC_WARP) {
+      // KeyCorridor's connect_all loop (mean 25, tail > 150 iterations) made
+      // one resetting lane the straggler of its tile and of the step.  When
+      // few lanes of the warp reset, the whole warp generates each of their
+      // levels in turn with 32 loop iterations per round; when many do (all
+      // random-policy episodes truncate together at T), one lane per level.
+      unsigned m = __ballot_sync(0xffffffffu, regen);
+      if (__popc(m) > KC_WARP_MAX) {
+        if (regen) o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi, a.gen_param);
+      } else {
+        while (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t ep_l = __shfl_sync(0xffffffffu, episode, l);
+          const uint32_t genv_l = __shfl_sync(0xffffffffu, genv, l);
+          const GenOut ol = generate_level<FAM, H, W, true>(RowViewT<RW>{rows - lane + l}, genv_l, ep_l, a.key_lo,
+                                                             a.key_hi, a.gen_param);
+          if (lane == l) o = ol;
+        }
+      }
+    } else {
+      o = generate_level<FAM, H, W>(g, genv, episode, a.key_lo, a.key_hi, a.gen_param);
+    }
+    if (regen) {
+      ax = o.ax; ay = o.ay; dir = o.dir;
+      target = o.target;
+      balls = o.balls;
+      st_fail = o.fail;
+      carry = CELL_EMPTY;
+      sc = 0;
+      prev_done = false;
+      grid_dirty = !grid_tmpl;
+      grid_tmpl = FAM == FAM_DYNOBS;
+    }
   }
   if (!regen) {
     if (FAM == FAM_DYNOBS) {
@@ -678,6 +709,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // small batches (<= 4 tiles per CTA): plain striding, no scheduler atomics
   // on the critical path; larger ones balance with the atomic counter
+  constexpr bool RESET_FIRST_FAM = FAM == FAM_KEYCORRIDOR;
   const bool stride_only = n_tiles <= 4 * (int64_t)gridDim.x;
   if (tid == 0) {
     mbar_init(smem_u32(&s_mbar[0]), 1);
@@ -697,7 +729,6 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   // the stamp reads and list atomics.
   // (striding, the small-batch mode, has no claim order to change: off there;
   // the mode is fixed for a handle, so the lists stay consistent)
-  constexpr bool RESET_FIRST_FAM = FAM == FAM_KEYCORRIDOR;
   const bool RESET_FIRST = RESET_FIRST_FAM && !stride_only;
   const uint32_t epoch = RESET_FIRST ? sched[2] : 0u;
   const uint32_t L = RESET_FIRST ? sched[3 + (epoch & 1u)] : 0u;

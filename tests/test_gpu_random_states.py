@@ -67,3 +67,33 @@ def test_import_rejects_illegal_records():
     with pytest.raises(NavixError):
         g.import_state(good[:1])
     np.testing.assert_array_equal(g.export_state(), good)  # rejected imports change nothing
+
+
+@pytest.mark.parametrize("env_id", ["KeyCorridorS3R3-v0", "KeyCorridorS3R1-v0", "KeyCorridorS4R3-v0",
+                                    "KeyCorridorS6R3-v0"])
+@pytest.mark.parametrize("p_prev_done", [0.03, 0.15])
+def test_keycorridor_sparse_resets_warp_generator(env_id, p_prev_done):
+    # random step counts desynchronise the episodes, so most steps reset a few
+    # lanes per warp: the warp-cooperative connect_all (<= 4 resetting lanes)
+    # and the one-lane-per-level path (more) both run, on the persistent
+    # (S3R*) and one-tile (S4R3, S6R3) kernels
+    from paper_2407_19396_b200 import NavixEnv
+    n = 2000
+    g = NavixEnv(env_id, n, seed=5)
+    s = g.spec
+    o = OracleEnv(env_id, n, seed=5)
+    recs = random_records(77, n, s.height, s.width, s.max_steps, 0, p_prev_done=p_prev_done)
+    g.import_state(recs)
+    o.import_(recs)
+    steps = 300 if s.height <= 7 else 60
+    acts = random_actions(9, steps, n, 0, high=8)
+    for t in range(steps):
+        go, gr, gte, gtr = g.step(torch.from_numpy(acts[t]).cuda())
+        oo, orw, ote, otr = o.step(acts[t])
+        np.testing.assert_array_equal(go.cpu().numpy(), oo, err_msg=f"obs step {t}")
+        np.testing.assert_array_equal(gr.cpu().numpy().view(np.uint32), orw.view(np.uint32))
+        np.testing.assert_array_equal(gte.cpu().numpy(), ote)
+        np.testing.assert_array_equal(gtr.cpu().numpy(), otr)
+        if t % 50 == 49:
+            np.testing.assert_array_equal(g.export_state(), o.export(), err_msg=f"state step {t}")
+    np.testing.assert_array_equal(g.stats().cpu().numpy(), o.stats())
