@@ -293,7 +293,8 @@ __device__ __forceinline__ void view_oob_walls(int ax, int ay, int dir, uint32_t
 }
 
 // process_vis of the 7x7 view (byte vj of vis_lo / vis_hi has bit vi set iff
-// view cell (vi, vj) is visible).
+// view cell (vi, vj) is visible; bit 7 of each byte is garbage — the callers
+// only ever move bit vi, vi <= 6, to a sign position).
 __device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const uint32_t (&chi)[7], uint32_t& vis_lo,
                                                 uint32_t& vis_hi) {
   // opacity rows: byte vj of op has bit vi set iff cell (vi, vj) is opaque
@@ -309,24 +310,28 @@ __device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const 
   const uint32_t tr_hi = (prmt(__brev(t_hi), 0u, 0x0123u) >> 1) & 0x7F7F7F7Fu;
   // rows vj = 6 .. 0 ([MG] process_vis order): V = R(S) | L(S), computed as
   // one carry chain on X = S | rev(S) << 8 over T2 = T | rev(T) << 8 (bit 7 = 0
-  // stops the carry between the halves)
+  // stops the carry between the halves).  The seed stays in that doubled form
+  // from row to row: dilation commutes with the reversal, so the next row's X
+  // is the dilated (V | rev(V) << 8) & T2, masked back to bits 0-6 / 8-14.
   vis_lo = 0;
   vis_hi = 0;
-  uint32_t seed = 1u << 3;  // bits 0-6 (bit 7 may hold garbage: the carry stopper absorbs it)
+  uint32_t x = (1u << 3) | (1u << 11);  // S = {vi = 3}, rev(S) = S
 #pragma unroll
   for (int j = 6; j >= 0; --j) {
     const uint32_t tw = j < 4 ? t_lo : t_hi, trw = j < 4 ? tr_lo : tr_hi;
     const uint32_t b = (uint32_t)(j & 3);
     // t2 = T | rev(T) << 8 (bits 7 and 15 zero: carry stoppers)
     const uint32_t t2 = prmt(tw, trw, 0x4400u | ((4u + b) << 4) | b) & 0x7F7Fu;
-    const uint32_t x = seed | (__brev(seed) >> 17);   // S | rev(S) << 8
     const uint32_t tx = t2 & x;
     const uint32_t v2 = x | ((t2 + tx) ^ (t2 ^ tx));  // R(S) | rev(L(S)) << 8 (carry chains)
-    const uint32_t v = (v2 | (__brev(v2) >> 17)) & 0x7Fu;
-    const uint32_t av = v & t2;
-    seed = av | (av << 1) | (av >> 1);
-    if (j < 4) vis_lo |= v << (8 * j);
-    else vis_hi |= v << (8 * (j - 4));
+    // V | rev(V) << 8 in bits 0-6 / 8-14 (bits 7 and 15: garbage)
+    const uint32_t w = v2 | (__brev(v2) >> 17);
+    const uint32_t av = w & t2;
+    x = (av | (av << 1) | (av >> 1)) & 0x7F7Fu;
+    // byte 0 of w into byte j of the row masks
+    const uint32_t sel = (0x3210u & ~(0xFu << (4 * b))) | (4u << (4 * b));
+    if (j < 4) vis_lo = prmt(vis_lo, w, sel);
+    else vis_hi = prmt(vis_hi, w, sel);
   }
 }
 
