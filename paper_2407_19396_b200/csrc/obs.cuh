@@ -320,14 +320,17 @@ __device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const 
   for (int j = 6; j >= 0; --j) {
     const uint32_t tw = j < 4 ? t_lo : t_hi, trw = j < 4 ? tr_lo : tr_hi;
     const uint32_t b = (uint32_t)(j & 3);
-    // t2 = T | rev(T) << 8 (bits 7 and 15 zero: carry stoppers)
-    const uint32_t t2 = prmt(tw, trw, 0x4400u | ((4u + b) << 4) | b) & 0x7F7Fu;
-    const uint32_t tx = t2 & x;
-    const uint32_t v2 = x | ((t2 + tx) ^ (t2 ^ tx));  // R(S) | rev(L(S)) << 8 (carry chains)
+    // t2 = T | rev(T) << 8 (bits 7 and 15 zero: carry stoppers; bytes 2-3
+    // zero: selector 8 replicates the sign of byte 0 of tw, which is 0)
+    const uint32_t t2 = prmt(tw, trw, 0x8800u | ((4u + b) << 4) | b);
+    // x may carry garbage in bits 7 and 15: t2 masks it out of the carry
+    // chains, and it only ever reaches bits 7 / 15 of v2 and w
+    const uint32_t sum = t2 + (t2 & x);
+    const uint32_t v2 = x | (sum ^ (t2 & ~x));  // R(S) | rev(L(S)) << 8 (carry chains)
     // V | rev(V) << 8 in bits 0-6 / 8-14 (bits 7 and 15: garbage)
     const uint32_t w = v2 | (__brev(v2) >> 17);
     const uint32_t av = w & t2;
-    x = (av | (av << 1) | (av >> 1)) & 0x7F7Fu;
+    x = av | (av << 1) | (av >> 1);
     // byte 0 of w into byte j of the row masks
     const uint32_t sel = (0x3210u & ~(0xFu << (4 * b))) | (4u << (4 * b));
     if (j < 4) vis_lo = prmt(vis_lo, w, sel);
