@@ -83,11 +83,13 @@ __device__ __forceinline__ void transpose4x4(uint32_t w0, uint32_t w1, uint32_t 
   o3 = __byte_perm(t2, t3, 0x7632);
 }
 
-__device__ __forceinline__ void transpose_lines(uint64_t* lines) {
+// (src == dst: in place; the rollout transposes into scratch lines, keeping
+// the rows for the next step)
+__device__ __forceinline__ void transpose_lines(const uint64_t* src, uint64_t* lines) {
   uint32_t lo[8], hi[8];
 #pragma unroll
   for (int y = 0; y < 8; ++y) {
-    const uint64_t r = lines[y * TILE];
+    const uint64_t r = src[y * TILE];
     lo[y] = (uint32_t)r;
     hi[y] = (uint32_t)(r >> 32);
   }
@@ -501,12 +503,10 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   const uint64_t* lines = rows;
   if (RW == 1 && (dir & 1)) {
     if (scratch) {
-#pragma unroll
-      for (int y = 0; y < 8; ++y) scratch[y * TILE] = rows[y * TILE];
-      transpose_lines(scratch);
+      transpose_lines(rows, scratch);
       lines = scratch;
     } else {
-      transpose_lines(rows);
+      transpose_lines(rows, rows);
     }
   }
   before_emit();
