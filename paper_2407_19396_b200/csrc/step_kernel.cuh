@@ -159,6 +159,7 @@ __device__ __forceinline__ bool issue_tile_loads(const KernelArgs& a, int64_t ti
 struct EnvResult {
   float reward;
   bool valid, regen, term, trunc, dirty;
+  bool tvalid;  // rollout: the scratch lines hold the transpose of the current rows
   uint64_t nrec, balls;
   uint32_t episode;
   uint32_t st[8];
@@ -172,6 +173,7 @@ struct EnvIn {
   uint64_t balls;    // DynObs ball positions (byte b = (x << 4) | y)
   uint32_t episode;  // episode counter
   bool episode_known;  // else read from HBM when an auto-reset needs it
+  bool tvalid;         // rollout: the scratch lines hold the transpose of these rows
 };
 
 template <int FAM, int MODE, int NPL>
@@ -501,9 +503,13 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
   const uint64_t* lines = rows;
+  // rollout: the transposed lines stay valid while the grid does not change
+  // (Dynamic-Obstacles moves its balls every step: never cached)
+  bool tvalid = FAM != FAM_DYNOBS && scratch != nullptr && in.tvalid && !grid_dirty;
   if (RW == 1 && (dir & 1)) {
     if (scratch) {
-      transpose_lines(rows, scratch);
+      if (!tvalid) transpose_lines(rows, scratch);
+      tvalid = FAM != FAM_DYNOBS;
       lines = scratch;
     } else {
       transpose_lines(rows, rows);
@@ -530,6 +536,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.term = term;
   r.trunc = trunc;
   r.dirty = grid_dirty;
+  r.tvalid = tvalid;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
            ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) |
            ((uint64_t)target << 56);
@@ -856,6 +863,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
     in.rec = r.nrec;
     in.episode = r.episode;
     in.balls = r.balls;
+    in.tvalid = r.tvalid;
     dirty |= r.dirty;
   }
   if (valid) {
