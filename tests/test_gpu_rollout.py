@@ -68,3 +68,30 @@ def test_rollout_random_policy_in_kernel(env_id, n, K, t0):
     for x, y in zip(ra, rb):
         assert torch.equal(x, y)
     np.testing.assert_array_equal(a.export_state(), b.export_state())
+
+
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "KeyCorridorS3R3-v0", "LavaGapS7-v0", "Empty-5x5-v0",
+                                    "GoToDoor-8x8-v0"])
+def test_rollout_dense_random_states_vs_oracle(env_id):
+    # imported random states (keys, balls, boxes, doors of every state near the
+    # agent): pickups, drops and toggles change the grid mid-rollout, so the
+    # rollout's cached transposed lines (odd directions) must be refreshed
+    # exactly when the grid changes
+    from paper_2407_19396_b200 import NavixEnv
+    from inputgen import random_records
+    n, K = 1500, 60
+    g = NavixEnv(env_id, n, seed=12)
+    o = OracleEnv(env_id, n, seed=12)
+    s = g.spec
+    recs = random_records(31, n, s.height, s.width, s.max_steps, 0, p_prev_done=0.02,
+                          open_edge=env_id.startswith("GoToDoor"))
+    g.import_state(recs)
+    o.import_(recs)
+    acts = random_actions(13, K, n, 0, high=7)
+    ro, rr, rte, rtr = g.rollout(torch.from_numpy(acts).cuda())
+    for t in range(K):
+        oo, orw, ote, otr = o.step(acts[t])
+        assert np.array_equal(ro[t].cpu().numpy(), oo), t
+        assert np.array_equal(rr[t].cpu().numpy().view(np.uint32), orw.view(np.uint32))
+        assert np.array_equal(rte[t].cpu().numpy(), ote) and np.array_equal(rtr[t].cpu().numpy(), otr)
+    assert np.array_equal(g.export_state(), o.export())
