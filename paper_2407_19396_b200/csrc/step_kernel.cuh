@@ -251,36 +251,44 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
   if (COMPACT) {
+    // The queue lives in staging this tile has consumed (decoded into
+    // registers before the first barrier below): the action bytes hold the
+    // queued slots, agent record st holds (episode | generator output << 32),
+    // DynObs ball word st the new balls; no static SMEM but the counter, so
+    // the kernel keeps the occupancy of the families without a queue.
     __shared__ int s_qn;
-    __shared__ int s_q[TILE];
-    __shared__ uint32_t s_qep[TILE];
-    __shared__ uint32_t s_qout[TILE];
-    __shared__ uint64_t s_qballs[TILE];
+    auto* const tb = reinterpret_cast<TileSmem<FAM, C::NPL>*>(rows - tid);
+    uint8_t* const q_slot = tb->act;
+    uint64_t* const q_rec = tb->agent;
+    uint64_t* const q_balls = tb->balls;
     if (tid == 0) s_qn = 0;
     __syncthreads();
     if (regen) {
-      s_q[atomicAdd(&s_qn, 1)] = tid;
-      s_qep[tid] = (in.episode_known ? episode : a.episode[slot]) + 1;
+      q_slot[atomicAdd(&s_qn, 1)] = (uint8_t)tid;
+      q_rec[tid] = (uint64_t)((in.episode_known ? episode : a.episode[slot]) + 1);
     }
     __syncthreads();
     const int nq = s_qn;
     for (int q = tid; q < nq; q += TILE) {
-      const int st = s_q[q];
+      const int st = q_slot[q];
       const uint32_t genv_t = a.env_begin + (uint32_t)(tile0 + env_of_slot(st));
-      const GenOut o =
-          generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, s_qep[st], a.key_lo, a.key_hi,
-                                    a.gen_param);
-      s_qballs[st] = FAM == FAM_GOTODOOR ? (uint64_t)o.target : o.balls;
-      s_qout[st] = (uint32_t)o.ax | ((uint32_t)o.ay << 8) | ((uint32_t)o.dir << 16) | (o.fail << 24);
+      const uint32_t ep = (uint32_t)q_rec[st];
+      const GenOut o = generate_level<FAM, H, W>(RowViewT<RW>{rows - tid + st}, genv_t, ep, a.key_lo, a.key_hi,
+                                                 a.gen_param);
+      if (FAM == FAM_DYNOBS) q_balls[st] = o.balls;
+      const uint32_t out = (uint32_t)o.ax | ((uint32_t)o.ay << 8) | ((uint32_t)o.dir << 16) |
+                           ((o.fail < 63u ? o.fail : 63u) << 18) | ((o.target & 0xFFu) << 24);
+      q_rec[st] = (uint64_t)ep | ((uint64_t)out << 32);
     }
     __syncthreads();
     if (regen) {
-      const uint32_t o = s_qout[tid];
-      episode = s_qep[tid];
-      if (FAM == FAM_GOTODOOR) target = (uint32_t)s_qballs[tid];
-      else balls = s_qballs[tid];
+      const uint64_t qr = q_rec[tid];
+      const uint32_t o = (uint32_t)(qr >> 32);
+      episode = (uint32_t)qr;
+      if (FAM == FAM_GOTODOOR) target = o >> 24;
+      else balls = q_balls[tid];
       ax = (int)(o & 0xFF); ay = (int)((o >> 8) & 0xFF); dir = (int)((o >> 16) & 3);
-      st_fail = o >> 24;
+      st_fail = (o >> 18) & 63u;
       carry = CELL_EMPTY;
       sc = 0;
       prev_done = false;
@@ -691,7 +699,8 @@ struct PersistSmem {
 };
 
 template <int FAM, int H, int W, int OBSK>
-__global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
+__global__ void __launch_bounds__(TILE, (FAM == FAM_GOTODOOR || FAM == FAM_DYNOBS ? 5 : 1))
+    navix_step_persistent(const KernelArgs a) {
   using C = Cfg<FAM, H, W>;
   auto& S = *reinterpret_cast<PersistSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
   uint8_t* const s_obs = S.obs;
