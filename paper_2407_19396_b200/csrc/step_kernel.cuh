@@ -699,8 +699,7 @@ struct PersistSmem {
 };
 
 template <int FAM, int H, int W, int OBSK>
-__global__ void __launch_bounds__(TILE, (FAM == FAM_GOTODOOR || FAM == FAM_DYNOBS ? 5 : 1))
-    navix_step_persistent(const KernelArgs a) {
+__global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a) {
   using C = Cfg<FAM, H, W>;
   auto& S = *reinterpret_cast<PersistSmem<FAM, C::NPL, OBSK>*>(navix_dyn_smem);
   uint8_t* const s_obs = S.obs;
