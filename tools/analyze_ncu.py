@@ -36,7 +36,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--so", default="paper_2407_19396_b200/libnavix.so")
-    ap.add_argument("--kernel", default="ILi1ELi8ELi8ELi0E")
+    ap.add_argument("--kernel", default="navix_step_persistentILi1ELi8ELi8ELi0E")  # the rollout / full-obs kernels share the template args
     ap.add_argument("--envs", type=int, default=1 << 20)
     ap.add_argument("--json")
     ap.add_argument("--lines", type=int, default=30)
