@@ -4,13 +4,16 @@ at 2^20 + 77 envs (dynamic tile scheduler, KeyCorridor's reset-first lists,
 PDL launches), then three 96-env blocks compared byte for byte with the CPU
 oracle replaying the same action stream.
 
-usage: PYTHONPATH=. python tools/soak.py
+usage: PYTHONPATH=. python tools/soak.py [env_id ...]
 """
 import sys, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2407_19396_b200 import NavixEnv
 from oracle import OracleEnv
-for env_id in ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "DoorKey-8x8-v0"]:
+ENVS = sys.argv[1:] or ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "DoorKey-8x8-v0", "GoToDoor-8x8-v0",
+                        "Dynamic-Obstacles-16x16-v0"]
+fail = False
+for env_id in ENVS:
     n = (1 << 20) + 77
     g = NavixEnv(env_id, n, seed=11)
     g.reset()
@@ -36,3 +39,7 @@ for env_id in ["KeyCorridorS3R3-v0", "Dynamic-Obstacles-8x8-v0", "DoorKey-8x8-v0
                 o.step(a[t])
         ok &= np.array_equal(o.export(), rec[b:b + 96])
     print(env_id, "2000 graph-replayed steps, sampled blocks equal oracle:", ok, flush=True)
+    fail |= not ok
+    del g, graph, acts
+    torch.cuda.empty_cache()
+sys.exit(1 if fail else 0)
