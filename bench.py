@@ -44,6 +44,16 @@ def measured_peaks():
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def step_kernel_name(env, env_id):
+    """The step kernel launch_fhwk (csrc/step_kernel.cuh) picks: the persistent
+    kernel for grids of at most 16 row planes (height x ceil(width / 8)), the
+    one-tile kernel above that (or when NAVIX_STEP_KERNEL selects it)."""
+    s = env.spec
+    planes = s.height * ((s.width + 7) // 8)
+    onetile = os.environ.get("NAVIX_STEP_KERNEL", "").startswith("o") or planes > 16
+    return f"navix_kernel<{env_id}, STEP>" if onetile else f"navix_step_persistent<{env_id}>"
+
+
 def committed_traffic(env_id: str):
     """dram bytes per env-step of the step kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -378,7 +388,7 @@ def run_navix(args, rank, world, local_rank):
     traffic = committed_traffic(args.env)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": None if traffic is None else traffic * n,
-            "algorithmic_bytes_per_env_step": B, "envs_per_launch": n, "kernel": f"navix_step_persistent<{args.env}>",
+            "algorithmic_bytes_per_env_step": B, "envs_per_launch": n, "kernel": step_kernel_name(env, args.env),
             "peak_source": peak_src}
     model, ncpu = cpu_info()
     cpu = None
