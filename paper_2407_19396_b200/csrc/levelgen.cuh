@@ -93,18 +93,31 @@ struct GenOut {
   uint32_t target;  // GoToDoor: target door (x << 4) | y
 };
 
-// k-th set bit of a multi-word mask (word w covers bits 64w ..).
+// bit p of a multi-word mask as word w's part (0 unless p is in word w), in
+// arithmetic form: an `if (w == p >> 6)` over unrolled words is turned back
+// into an indexed store by the compiler, which moves the mask to local memory.
+__device__ __forceinline__ uint64_t word_bit(int p, int w) {
+  const unsigned d = (unsigned)(p - 64 * w);
+  return (uint64_t)(d < 64u) << (d & 63u);
+}
+
+// k-th set bit of a multi-word mask (word w covers bits 64w ..), -1 if fewer.
+// The word holding it is picked with selects over the unrolled words (no early
+// return, no dynamic index), so the mask stays in registers: an early-exit
+// loop put the DynObs-16x16 free-cell mask in local memory (LDL/STL).
 template <int NW>
 __device__ __forceinline__ int select_bits(const uint64_t (&m)[NW], uint32_t k) {
-  int base = 0;
+  uint64_t word = 0;
+  int base = -1;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     const uint32_t c = __popcll(m[w]);
-    if (k < c) return base + select64(m[w], k);
-    k -= c;
-    base += 64;
+    const bool here = base < 0 && k < c;
+    word = here ? m[w] : word;
+    base = here ? 64 * w : base;
+    k = (base < 0) ? k - c : k;
   }
-  return -1;
+  return base < 0 ? -1 : base + select64(word, k);
 }
 
 // word t (0..7) of the two consecutive Philox blocks (x0, x1)
@@ -310,7 +323,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       const int ab = o.ay * RSB + o.ax;  // the agent's cell
 #pragma unroll
       for (int w = 0; w < NWD; ++w)
-        if (w == (ab >> 6)) freem[w] &= ~(1ull << (ab & 63));
+        freem[w] &= ~word_bit(ab, w);
     }
 #pragma unroll
     for (int b = 0; b < C::NOBST; ++b) {
@@ -323,8 +336,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       if constexpr (NWD == 1) freem[0] &= ~(1ull << pos);
       else {
 #pragma unroll
-        for (int w = 0; w < NWD; ++w)
-          if (w == (pos >> 6)) freem[w] &= ~(1ull << (pos & 63));
+        for (int w = 0; w < NWD; ++w) freem[w] &= ~word_bit(pos, w);
       }
       const int x = pos % RSB, y = pos / RSB;
       g.set(x, y, make_cell(K_BALL, COL_BLUE));
