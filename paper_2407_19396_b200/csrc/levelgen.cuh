@@ -347,12 +347,16 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     constexpr int S = C::RS, NR = C::NR, NC = 3, NROOM = NR * NC;
     // door_pos[0].y (right wall) and door_pos[1].x (bottom wall) per room,
     // drawn room by room (j outer, i inner) as [MG] does
-    uint8_t dpy[NROOM], dpx[NROOM];
+    // nibble r of dpy / dpx = room r's door position (< 16 on grids of at most
+    // 17 cells; registers, not a dynamically indexed local array)
+    static_assert(H <= 17 && W <= 17 && NROOM <= 16, "door positions are packed in nibbles");
+    uint64_t dpy = 0, dpx = 0;
+    auto nib = [](uint64_t w, int r) { return (int)((w >> (4 * r)) & 15u); };
     for (int j = 0; j < NR; ++j)
       for (int i = 0; i < NC; ++i) {
         const int r = j * NC + i;
-        if (i < NC - 1) dpy[r] = (uint8_t)(j * (S - 1) + 1 + ds.next_bounded(S - 2));
-        if (j < NR - 1) dpx[r] = (uint8_t)(i * (S - 1) + 1 + ds.next_bounded(S - 2));
+        if (i < NC - 1) dpy |= (uint64_t)(j * (S - 1) + 1 + ds.next_bounded(S - 2)) << (4 * r);
+        if (j < NR - 1) dpx |= (uint64_t)(i * (S - 1) + 1 + ds.next_bounded(S - 2)) << (4 * r);
       }
     // room links as bit masks over rooms r = 3j + i: H bit r = rooms r, r+1
     // linked; V bit r = rooms r, r+3 linked (removed walls and doors of any state)
@@ -366,7 +370,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     const int room_idx = (int)ds.next_bounded(NR);
     const uint8_t door_col = (uint8_t)ds.next_bounded(6);           // R#23
     const int locked_room = room_idx * NC + 2;
-    g.set(2 * (S - 1), dpy[room_idx * NC + 1], make_cell(K_DOOR_LOCKED, door_col));
+    g.set(2 * (S - 1), nib(dpy, room_idx * NC + 1), make_cell(K_DOOR_LOCKED, door_col));
     Hl |= 1u << (locked_room - 1);
     // object placement inside room (ri, rj): empty, not the default agent
     // cell, Manhattan distance >= 2 from it (reject_next_to, R#25)
@@ -469,8 +473,8 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
         const bool fh = __shfl_sync(0xffffffffu, (int)horiz, f) != 0;
         const uint8_t col = (uint8_t)bounded(__shfl_sync(0xffffffffu, wc, f), 6);
         const int li = flo % NC, lj = flo / NC;
-        const int x = fh ? li * (S - 1) + S - 1 : dpx[flo];
-        const int y = fh ? dpy[flo] : lj * (S - 1) + S - 1;
+        const int x = fh ? li * (S - 1) + S - 1 : nib(dpx, flo);
+        const int y = fh ? nib(dpy, flo) : lj * (S - 1) + S - 1;
         g.set(x, y, make_cell(K_DOOR_CLOSED, col));
         if (fh) Hl |= 1u << flo;
         else Vl |= 1u << flo;
@@ -496,8 +500,8 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       if (r == locked_room || nb == locked_room) continue;
       const uint8_t col = (uint8_t)ds.next_bounded(6);
       const int li = lo % NC, lj = lo / NC;
-      const int x = horiz ? li * (S - 1) + S - 1 : dpx[lo];
-      const int y = horiz ? dpy[lo] : lj * (S - 1) + S - 1;
+      const int x = horiz ? li * (S - 1) + S - 1 : nib(dpx, lo);
+      const int y = horiz ? nib(dpy, lo) : lj * (S - 1) + S - 1;
       g.set(x, y, make_cell(K_DOOR_CLOSED, col));
       if (horiz) Hl |= 1u << lo;
       else Vl |= 1u << lo;
