@@ -412,7 +412,11 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
             const uint8_t f = g.get(fx, fy);
             const bool ok = f == CELL_EMPTY || (f & 15) == K_WALL;
             const int bit = (yy * S + xx) * 4 + d;
-            m[bit >> 6] |= (ok ? 1ull : 0ull) << (bit & 63);
+            if constexpr (NWD == 1) m[0] |= (ok ? 1ull : 0ull) << bit;
+            else {  // no m[bit >> 6]: a dynamic index puts m in local memory
+#pragma unroll
+              for (int w = 0; w < NWD; ++w) m[w] |= ok ? word_bit(bit, w) : 0ull;
+            }
             n += ok;
           }
         }
