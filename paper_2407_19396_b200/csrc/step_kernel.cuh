@@ -247,7 +247,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // them), each into its env's SMEM rows.
   // (measured: the queue pays on the narrow persistent kernel, not on the
   // 16x16 one-tile kernel, where it costs 8 % at 2^20 and 50 % at 2^16 envs)
-  constexpr bool COMPACT = ((FAM == FAM_DYNOBS && RW == 1) || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
+  constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
   if (COMPACT) {
