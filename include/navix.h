@@ -88,9 +88,12 @@ typedef struct {
 
 /* Parse an id such as "Navix-DoorKey-8x8-v0", "MiniGrid-DoorKey-8x8-v0" or
  * "DoorKey-8x8" (Code 1 P:254).  Host only; no CUDA call.
- * Returns NAVIX_E_UNKNOWN_ENV for ids outside Table 9 (and MiniGrid's
- * Dynamic-Obstacles-Random / SimpleCrossing spellings, R#35, R#40).  Every
- * Table 9 id has a kernel. */
+ * Returns NAVIX_E_UNKNOWN_ENV for ids outside Table 8 / Table 9 (P:858-893,
+ * P:908-965) and MiniGrid's Dynamic-Obstacles-Random / LavaCrossing spellings
+ * (R#35, R#40).  Both tables' spellings are accepted: "LavaGapS7" (Table 8) and
+ * "LavaGap-S7" (Table 9); "SimpleCrossingS9N1" (Table 8: wall rivers) and
+ * "Crossings-S9N1" (Table 9, reward R_2: lava rivers, = MiniGrid's
+ * "LavaCrossingS9N1").  Every Table 8 / Table 9 id has a kernel. */
 NAVIX_API navix_status navix_spec_of(const char* env_id, navix_spec* out);
 
 /* Bytes of device state for `num_envs` envs of `env_id` (for a caller-owned

@@ -121,7 +121,8 @@ static void gen_distshift(Env& e) {
 }
 
 // ---------------------------------------------------------------- Crossing
-// [MG] CrossingEnv._gen_grid with obstacle_type = Wall, step by step.  The two
+// [MG] CrossingEnv._gen_grid with obstacle_type = Wall (SimpleCrossing) or
+// Lava (Table 9's Crossings, LavaCrossing; R#35), step by step.  The two
 // np_random.shuffle calls follow R#35: the rivers list is shuffled by a
 // partial Fisher-Yates over its first num_crossings slots (slot k swaps with
 // k + bounded(draw, M - k)), which is all [MG] keeps of it; the path is
@@ -148,10 +149,11 @@ static void gen_crossing(Env& e, DrawStream& ds) {
   std::sort(rivers_v.begin(), rivers_v.end());
   std::sort(rivers_h.begin(), rivers_h.end());
   // obstacle_pos = product(range(1, W-1), rivers_h) ++ product(rivers_v, range(1, H-1))
+  const Obj obstacle = e.spec.lava_obstacle ? make_lava() : make_wall();
   for (int i = 1; i < W - 1; ++i)
-    for (int j : rivers_h) e.grid.set(i, j, make_wall());
+    for (int j : rivers_h) e.grid.set(i, j, obstacle);
   for (int i : rivers_v)
-    for (int j = 1; j < H - 1; ++j) e.grid.set(i, j, make_wall());
+    for (int j = 1; j < H - 1; ++j) e.grid.set(i, j, obstacle);
   // path = [h] * len(rivers_v) + [v] * len(rivers_h), shuffled
   std::vector<char> path;
   for (size_t k = 0; k < rivers_v.size(); ++k) path.push_back('h');

@@ -198,10 +198,14 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     s.strip2_row = id == "DistShift1" ? 2 : 5;
     s.max_steps = 4 * 9 * 7;
     s.n_actions = 7;
-  } else if (starts_with(id, "SimpleCrossingS") || starts_with(id, "Crossings-S")) {
-    // [MG] CrossingEnv(size, num_crossings, obstacle_type=Wall); Table 9 also
-    // spells it "Crossings-S9N1" (R#35)
-    pos = starts_with(id, "SimpleCrossingS") ? 15 : 11;
+  } else if (starts_with(id, "SimpleCrossingS") || starts_with(id, "Crossings-S") ||
+             starts_with(id, "LavaCrossingS")) {
+    // [MG] CrossingEnv(size, num_crossings, obstacle_type): Table 8's
+    // SimpleCrossing ids have wall rivers; Table 9's
+    // "Crossings-S9N1" ids carry R_2, read as [MG]'s
+    // LavaCrossing, obstacle_type=Lava (R#35)
+    s.lava_obstacle = !starts_with(id, "SimpleCrossingS");
+    pos = starts_with(id, "SimpleCrossingS") ? 15 : starts_with(id, "LavaCrossingS") ? 13 : 11;
     int S, N;
     if (!parse_int(id, pos, &S)) return false;
     if (pos >= id.size() || id[pos] != 'N') return false;
@@ -247,8 +251,9 @@ bool parse_env_id(const std::string& id_in, Spec* out) {
     int n = s.size == 5 ? 2 : s.size == 6 ? 3 : s.size == 16 ? 8 : 4;
     if (!(n <= s.size / 2.0 + 1)) n = s.size / 2;
     s.n_obstacles = n;
-  } else if (starts_with(id, "LavaGapS")) {
-    pos = 8;
+  } else if (starts_with(id, "LavaGapS") || starts_with(id, "LavaGap-S")) {
+    // Table 8 spells it LavaGapS7, Table 9 LavaGap-S7
+    pos = starts_with(id, "LavaGapS") ? 8 : 9;
     int S;
     if (!parse_int(id, pos, &S) || pos != id.size()) return false;
     if (S < 5 || S > 16) return false;

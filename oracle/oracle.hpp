@@ -95,6 +95,7 @@ struct Spec {
   int n_obstacles;    // DynObs
   int strip2_row;     // DistShift
   int n_crossings;    // SimpleCrossing N
+  bool lava_obstacle;  // Crossings: lava rivers (Table 9 R_2, LavaCrossing) instead of walls
   bool random_start;  // Dynamic-Obstacles-Random: place_agent() instead of (1,1) east
 };
 // Parses "Navix-DoorKey-8x8-v0" / "MiniGrid-…" / bare ids. false if unknown.

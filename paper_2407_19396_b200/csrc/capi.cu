@@ -95,9 +95,13 @@ int parse_id(const char* env_id, EnvConfig* c) {
   } else if (id == "DistShift1" || id == "DistShift2") {  // [MG] DistShiftEnv 9x7 (R#33)
     *c = EnvConfig{id == "DistShift1" ? FAM_DISTSHIFT1 : FAM_DISTSHIFT2, 7, 9, 4 * 9 * 7, 7, 0, 0, 0};
   } else if (sscanf(id.c_str(), "SimpleCrossingS%dN%d%c", &a, &b, &tail) == 2 ||
-             sscanf(id.c_str(), "Crossings-S%dN%d%c", &a, &b, &tail) == 2) {  // [MG] CrossingEnv (R#35)
+             sscanf(id.c_str(), "Crossings-S%dN%d%c", &a, &b, &tail) == 2 ||
+             sscanf(id.c_str(), "LavaCrossingS%dN%d%c", &a, &b, &tail) == 2) {
+    // [MG] CrossingEnv (R#35): Table 8's SimpleCrossing = wall rivers;
+    // Table 9's Crossings (R_2) = [MG]'s LavaCrossing, lava rivers
     if (!((a == 9 && b >= 1 && b <= 3) || (a == 11 && b == 5))) return 1;
-    *c = EnvConfig{FAM_CROSSING, a, a, 4 * a * a, 7, 0, 0, 0, b};
+    const int lava = id.rfind("SimpleCrossingS", 0) == 0 ? 0 : CROSSING_LAVA;
+    *c = EnvConfig{FAM_CROSSING, a, a, 4 * a * a, 7, 0, 0, 0, b | lava};
   } else if (id == "FourRooms") {  // [MG] FourRoomsEnv at Table 9's 17x17, max_steps 100 (R#38)
     *c = EnvConfig{FAM_FOURROOMS, 17, 17, 100, 7, 0, 0, 0};
   } else if (sq("GoToDoor-%dx%d%c")) {  // [MG] GoToDoorEnv (R#37)
@@ -114,7 +118,8 @@ int parse_id(const char* env_id, EnvConfig* c) {
     const int nob = a == 5 ? 2 : a == 6 ? 3 : a == 8 ? 4 : 8;  // R#6
     const int random_start = id.find("-Random-") != std::string::npos;  // R#40
     *c = EnvConfig{FAM_DYNOBS, a, a, 4 * a * a, 3, nob, 0, 0, random_start};
-  } else if (sscanf(id.c_str(), "LavaGapS%d%c", &a, &tail) == 1) {
+  } else if (sscanf(id.c_str(), "LavaGapS%d%c", &a, &tail) == 1 ||
+             sscanf(id.c_str(), "LavaGap-S%d%c", &a, &tail) == 1) {  // Table 8 / Table 9 spellings
     if (a < 5 || a > 7) return 1;
     *c = EnvConfig{FAM_LAVAGAP, a, a, 4 * a * a, 7, 0, 0, 0};
   } else if (sscanf(id.c_str(), "KeyCorridorS%dR%d%c", &a, &b, &tail) == 2) {

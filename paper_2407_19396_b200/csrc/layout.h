@@ -68,8 +68,9 @@ struct EnvConfig {
   int n_actions;
   int n_obstacles;
   int room_size, num_rows;  // KeyCorridor
-  int gen_param;            // SimpleCrossing: number of crossings N
+  int gen_param;            // Crossing: number of crossings N | CROSSING_LAVA
 };
+constexpr int CROSSING_LAVA = 0x100;  // gen_param bit: lava rivers (Table 9 Crossings / LavaCrossing, R#35)
 
 // Byte offsets of the arrays inside one state allocation.
 struct StateLayout {

@@ -229,11 +229,13 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     const int ty = t == 0 ? 0 : t == 1 ? h - 1 : t == 2 ? d2 : d3;
     o.target = (uint32_t)((tx << 4) | ty);
   } else if constexpr (FAM == FAM_CROSSING) {
-    // [MG] CrossingEnv._gen_grid, obstacle Wall, N = gparam crossings; the two
+    // [MG] CrossingEnv._gen_grid, obstacle Wall or Lava (gparam & CROSSING_LAVA),
+    // N = gparam & 0xff crossings; the two
     // shuffles as R#35 reads them.  Rivers are nibbles (bit 3: horizontal,
     // bits 0-2: position / 2 - 1): (S-3)/2 vertical ones, then as many horizontal.
     constexpr int NRV = (W - 3) / 2, M = 2 * NRV;
-    const int N = gparam;
+    const int N = gparam & 0xff;
+    const uint8_t obstacle = (gparam & CROSSING_LAVA) ? CELL_LAVA : CELL_WALL;
     uint64_t riv = 0;
 #pragma unroll
     for (int k = 0; k < M; ++k) riv |= (uint64_t)((k < NRV ? 0 : 8) | (k % NRV)) << (4 * k);
@@ -249,7 +251,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     for (int y = 1; y < H - 1; ++y)
 #pragma unroll
       for (int x = 1; x < W - 1; ++x)
-        if (((hmask >> y) & 1u) | ((vmask >> x) & 1u)) g.set(x, y, CELL_WALL);
+        if (((hmask >> y) & 1u) | ((vmask >> x) & 1u)) g.set(x, y, obstacle);
     // path: popc(vmask) 'h' moves then popc(hmask) 'v' moves (bit k = 1: 'v'), Fisher-Yates
     const int nv = __popc(vmask);
     uint32_t path = ((1u << N) - 1) & ~((1u << nv) - 1);

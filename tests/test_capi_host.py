@@ -33,6 +33,10 @@ def test_header_symbols_are_exported():
     ("Navix-DistShift2-v0", 7, 9, 252, 7, 6),
     ("Navix-SimpleCrossingS9N2-v0", 9, 9, 324, 7, 7),
     ("Navix-Crossings-S11N5-v0", 11, 11, 484, 7, 7),
+    ("Navix-Crossings-S9N1-v0", 9, 9, 324, 7, 7),
+    ("MiniGrid-LavaCrossingS9N2-v0", 9, 9, 324, 7, 7),
+    ("Navix-LavaGap-S7-v0", 7, 7, 196, 7, 4),
+    ("Navix-LavaGap-S5-v0", 5, 5, 100, 7, 4),
     ("Navix-DoorKey-Random-5x5", 5, 5, 250, 7, 1),
     ("Navix-GoToDoor-8x8-v0", 8, 8, 256, 7, 8),
     ("Navix-FourRooms-v0", 17, 17, 100, 7, 9),
@@ -103,7 +107,9 @@ def test_every_id_the_library_accepts_the_oracle_parses_identically():
     fams = ["Empty-{s}x{s}", "Empty-Random-{s}x{s}", "DoorKey-{s}x{s}", "DoorKey-Random-{s}x{s}",
             "Dynamic-Obstacles-{s}x{s}", "Dynamic-Obstacles-Random-{s}x{s}", "LavaGapS{s}", "GoToDoor-{s}x{s}",
             "KeyCorridorS{s}R1", "KeyCorridorS{s}R2", "KeyCorridorS{s}R3", "SimpleCrossingS{s}N1",
-            "SimpleCrossingS{s}N2", "SimpleCrossingS{s}N3", "SimpleCrossingS{s}N5", "Crossings-S{s}N5"]
+            "SimpleCrossingS{s}N2", "SimpleCrossingS{s}N3", "SimpleCrossingS{s}N5", "Crossings-S{s}N1",
+            "Crossings-S{s}N2", "Crossings-S{s}N3", "Crossings-S{s}N5", "LavaCrossingS{s}N1", "LavaCrossingS{s}N2",
+            "LavaCrossingS{s}N3", "LavaCrossingS{s}N5", "LavaGap-S{s}"]
     extra = ["FourRooms", "DistShift1", "DistShift2"]
     accepted = 0
     for pre in ("", "Navix-", "MiniGrid-"):
@@ -118,6 +124,43 @@ def test_every_id_the_library_accepts_the_oracle_parses_identically():
                 o = oracle_spec(env_id)
                 assert (o.height, o.width, o.max_steps, o.n_actions, o.family, o.export_bytes, o.n_obstacles) == \
                     (s.height, s.width, s.max_steps, s.n_actions, s.family, s.export_bytes, s.n_obstacles), env_id
-    # 44 kernel-backed ids (every Table 9 id, plus DoorKey / Dynamic-Obstacles
-    # -Random at every size and both Crossing spellings) x 6 spellings
-    assert accepted == 6 * 44
+    # 54 kernel-backed ids (every Table 8 / 9 id, plus DoorKey / Dynamic-Obstacles
+    # -Random at every size, the three Crossing and two LavaGap spellings) x 6 spellings
+    assert accepted == 6 * 54
+
+
+# Every env id printed in Table 8 and Table 9, verbatim
+# (the duplicated Dynamic-Obstacles rows and the stray "N" of P:952 dropped, R#26).
+TABLE8 = ["Navix-Empty-5x5-v0", "Navix-Empty-6x6-v0", "Navix-Empty-8x8-v0", "Navix-Empty-16x16-v0",
+          "Navix-Empty-Random-5x5", "Navix-Empty-Random-6x6", "Navix-DoorKey-5x5-v0", "Navix-DoorKey-6x6-v0",
+          "Navix-DoorKey-8x8-v0", "Navix-DoorKey-16x16-v0", "Navix-FourRooms-v0", "Navix-KeyCorridorS3R1-v0",
+          "Navix-KeyCorridorS3R2-v0", "Navix-KeyCorridorS3R3-v0", "Navix-KeyCorridorS4R3-v0",
+          "Navix-KeyCorridorS5R3-v0", "Navix-KeyCorridorS6R3-v0", "Navix-LavaGapS5-v0", "Navix-LavaGapS6-v0",
+          "Navix-LavaGapS7-v0", "Navix-SimpleCrossingS9N1-v0", "Navix-SimpleCrossingS9N2-v0",
+          "Navix-SimpleCrossingS9N3-v0", "Navix-SimpleCrossingS11N5-v0", "Navix-Dynamic-Obstacles-5x5",
+          "Navix-Dynamic-Obstacles-6x6", "Navix-Dynamic-Obstacles-8x8", "Navix-Dynamic-Obstacles-16x16",
+          "Navix-DistShift1-v0", "Navix-DistShift2-v0"]
+TABLE9 = ["Navix-Empty-5x5-v0", "Navix-Empty-6x6-v0", "Navix-Empty-8x8-v0", "Navix-Empty-16x16-v0",
+          "Navix-Empty-Random-5x5", "Navix-Empty-Random-6x6", "Navix-Empty-Random-8x8", "Navix-Empty-Random-16x16",
+          "Navix-DoorKey-5x5-v0", "Navix-DoorKey-6x6-v0", "Navix-DoorKey-8x8-v0", "Navix-DoorKey-16x16-v0",
+          "Navix-DoorKey-Random-5x5", "Navix-DoorKey-Random-6x6", "Navix-DoorKey-Random-8x8",
+          "Navix-DoorKey-Random-16x16", "Navix-FourRooms-v0", "Navix-KeyCorridorS3R1-v0", "Navix-KeyCorridorS3R2-v0",
+          "Navix-KeyCorridorS3R3-v0", "Navix-KeyCorridorS4R3-v0", "Navix-KeyCorridorS5R3-v0",
+          "Navix-KeyCorridorS6R3-v0", "Navix-LavaGap-S5-v0", "Navix-LavaGap-S6-v0", "Navix-LavaGap-S7-v0",
+          "Navix-Crossings-S9N1-v0", "Navix-Crossings-S9N2-v0", "Navix-Crossings-S9N3-v0", "Navix-Crossings-S11N5-v0",
+          "Navix-Dynamic-Obstacles-5x5", "Navix-Dynamic-Obstacles-6x6", "Navix-Dynamic-Obstacles-8x8",
+          "Navix-Dynamic-Obstacles-16x16", "Navix-DistShift1-v0", "Navix-DistShift2-v0", "Navix-GoToDoor-5x5-v0",
+          "Navix-GoToDoor-6x6-v0", "Navix-GoToDoor-8x8-v0"]
+
+
+@pytest.mark.parametrize("env_id", sorted(set(TABLE8 + TABLE9)))
+def test_every_table8_table9_id_has_a_kernel(env_id):
+    # navix_spec_of returns NAVIX_OK only for ids with a kernel instantiation
+    # (NAVIX_E_UNSUPPORTED otherwise); the oracle parses the same spec
+    from oracle import spec_of as oracle_spec
+    from paper_2407_19396_b200 import load_library
+    from paper_2407_19396_b200.navix import _Spec
+    s = _Spec()
+    assert load_library().navix_spec_of(env_id.encode(), ctypes.byref(s)) == 0, env_id
+    o = oracle_spec(env_id)
+    assert (o.height, o.width, o.max_steps) == (s.height, s.width, s.max_steps)

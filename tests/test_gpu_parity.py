@@ -219,7 +219,9 @@ def test_cuda_graph_replay_matches_eager():
                                     "SimpleCrossingS9N1-v0", "SimpleCrossingS9N2-v0", "SimpleCrossingS9N3-v0",
                                     "SimpleCrossingS11N5-v0", "DoorKey-Random-8x8", "GoToDoor-5x5-v0",
                                     "GoToDoor-6x6-v0", "GoToDoor-8x8-v0", "FourRooms-v0",
-                                    "Dynamic-Obstacles-Random-5x5", "Dynamic-Obstacles-Random-6x6"])
+                                    "Dynamic-Obstacles-Random-5x5", "Dynamic-Obstacles-Random-6x6",
+                                    "Navix-Crossings-S9N1-v0", "Navix-Crossings-S9N2-v0", "Navix-Crossings-S9N3-v0",
+                                    "Navix-Crossings-S11N5-v0", "Navix-LavaGap-S7-v0"])
 def test_parity_row_f2_more_families(env_id):
     # Empty-Random (random start cell + direction per episode) and DistShift (9x7, lava strips)
     run_parity(env_id, 555, 600, block=555, seed=21)

@@ -1,6 +1,8 @@
 """Pins of the oracle's further Table 9 families (row f2):
 Empty-Random-SxS and DistShift1/2 (Table 9; MiniGrid's EmptyEnv with
-agent_start_pos=None and DistShiftEnv; R#33, R#34).
+agent_start_pos=None and DistShiftEnv; R#33, R#34); the Crossings (Table 8's
+SimpleCrossing with wall rivers, Table 9's Crossings with R_2 = MiniGrid's
+LavaCrossing, lava rivers; R#35); GoToDoor, FourRooms, DynObs-Random.
 
 DistShift: the layout the MiniGrid source fixes (goal (W-2, 1), lava strips
 x = 3..W-4 on rows 1 and 2 (DistShift1) or 5 (DistShift2), agent (1,1) east)
@@ -138,18 +140,20 @@ def _reachable(t, sx, sy):
     return seen
 
 
-@pytest.mark.parametrize("env_id,S,N", [("SimpleCrossingS9N1-v0", 9, 1), ("SimpleCrossingS9N2-v0", 9, 2),
-                                        ("SimpleCrossingS9N3-v0", 9, 3), ("Crossings-S11N5-v0", 11, 5)])
-def test_crossing_structure_and_solvable(env_id, S, N):
+@pytest.mark.parametrize("env_id,S,N,ob", [("SimpleCrossingS9N1-v0", 9, 1, 2), ("SimpleCrossingS9N2-v0", 9, 2, 2),
+                                           ("SimpleCrossingS9N3-v0", 9, 3, 2), ("SimpleCrossingS11N5-v0", 11, 5, 2),
+                                           ("Crossings-S9N1-v0", 9, 1, 9), ("Navix-Crossings-S9N3-v0", 9, 3, 9),
+                                           ("Crossings-S11N5-v0", 11, 5, 9), ("LavaCrossingS9N2-v0", 9, 2, 9)])
+def test_crossing_structure_and_solvable(env_id, S, N, ob):
     s = spec_of(env_id)
     assert (s.width, s.height, s.max_steps, s.n_actions) == (S, S, 4 * S * S, 7)
     levels = _crossing_levels(env_id, 400)
     for t in levels:
         assert t[1, 1] == 10 and t[S - 2, S - 2] == 8
-        # a river line holds S-3 walls (its one opening excepted); any other
-        # interior line holds at most N walls (where rivers cross it) < S-3
-        cols = [x for x in range(1, S - 1) if np.count_nonzero(t[x, 1:-1] == 2) == S - 3]
-        rows = [y for y in range(1, S - 1) if np.count_nonzero(t[1:-1, y] == 2) == S - 3]
+        # a river line holds S-3 obstacles (its one opening excepted); any other
+        # interior line holds at most N obstacles (where rivers cross it) < S-3
+        cols = [x for x in range(1, S - 1) if np.count_nonzero(t[x, 1:-1] == ob) == S - 3]
+        rows = [y for y in range(1, S - 1) if np.count_nonzero(t[1:-1, y] == ob) == S - 3]
         assert all(x % 2 == 0 and 2 <= x <= S - 3 for x in cols)
         assert all(y % 2 == 0 and 2 <= y <= S - 3 for y in rows)
         assert len(cols) + len(rows) == N
@@ -159,10 +163,57 @@ def test_crossing_structure_and_solvable(env_id, S, N):
         for y in rows:
             want[1:-1, y] = True
         interior = np.pad(np.ones((S - 2, S - 2), bool), 1)
-        got = t == 2
-        assert not np.any(got & interior & ~want)      # no wall off the rivers
+        got = t == ob
+        assert not np.any(interior & (t == (9 if ob == 2 else 2)))  # one obstacle kind only
+        assert not np.any(got & interior & ~want)      # no obstacle off the rivers
         assert np.count_nonzero(want & ~got) == N      # exactly one opening per river
-        assert _reachable(t, 1, 1)[S - 2, S - 2]       # the openings connect start and goal
+        assert _reachable(np.where(t == 9, 2, t), 1, 1)[S - 2, S - 2]  # openings connect start and goal
+
+
+@pytest.mark.parametrize("S,N", [(9, 1), (9, 2), (9, 3), (11, 5)])
+def test_lava_crossing_is_simple_crossing_with_lava(S, N):
+    # the same draws build the same rivers and openings; only the obstacle differs
+    simple = _crossing_levels(f"SimpleCrossingS{S}N{N}-v0", 300, seed=4)
+    for lava_id in (f"Crossings-S{S}N{N}-v0", f"LavaCrossingS{S}N{N}-v0"):
+        lava = _crossing_levels(lava_id, 300, seed=4)
+        inner = np.zeros((S, S), bool)
+        inner[1:-1, 1:-1] = True
+        want = np.where((simple == 2) & inner[None], 9, simple)
+        assert np.array_equal(lava, want)
+
+
+def test_lava_crossing_terminates_on_lava_and_sees_across():
+    # Table 9 R_2 (caption P:972): "-1 when the agent is on the lava
+    # square"; all envs terminate when the reward is not 0; MiniGrid's
+    # lava pays 0 (R#3).  A vertical lava river at x = 2 with its opening at (2,5).
+    m = ["#########",
+         "#AV.....#",
+         "#.V.....#",
+         "#.V.....#",
+         "#.V.....#",
+         "#.......#",
+         "#.V.....#",
+         "#.V....G#",
+         "#########"]
+    for mode, want in ((0, 0.0), (1, -1.0)):
+        env = OracleEnv("Crossings-S9N1-v0", 1, seed=0, reward_mode=mode)
+        env.reset()
+        env.import_(record_from_map(m, 0).reshape(1, -1))
+        obs = env.observe()[0]
+        # lava is see-through (MiniGrid Lava.see_behind): the cells beyond the
+        # river are visible, e.g. (3,1) = view (vi=3, vj=4) facing east
+        assert obs[3, 4].tolist() == [1, 0, 0] and obs[3, 5].tolist() == [9, 0, 0]
+        _, r, te, tr = env.step(np.array([F], np.uint8))
+        assert te[0] == 1 and tr[0] == 0 and float(r[0]) == want
+        assert env.stats()[4] == 1
+    # the same map with wall rivers (SimpleCrossing): the river occludes
+    env = OracleEnv("SimpleCrossingS9N1-v0", 1, seed=0)
+    env.reset()
+    env.import_(record_from_map([r.replace("V", "#") for r in m], 0).reshape(1, -1))
+    obs = env.observe()[0]
+    assert obs[3, 5].tolist() == [2, 5, 0] and obs[3, 4].tolist() == [0, 0, 0]
+    _, r, te, _ = env.step(np.array([F], np.uint8))
+    assert te[0] == 0 and r[0] == 0
 
 
 def test_crossing_river_subset_and_opening_uniform():

@@ -61,9 +61,9 @@ def test_invariants_random_rollout(env_id):
             n_keys = np.count_nonzero(ty == KEY) + (carry[0] == KEY)
             n_keys0 = np.count_nonzero(pc[:, :, 0] == KEY) + (prev[e, p + 3] == KEY)
             assert n_keys == n_keys0
-            if s.family != 2:  # balls move in DynObs
-                n_b = np.count_nonzero(ty == BALL) + (carry[0] == BALL)
-                assert n_b == np.count_nonzero(pc[:, :, 0] == BALL) + (prev[e, p + 3] == BALL)
+            # balls are conserved too in DynObs, where they move (grid + pocket)
+            n_b = np.count_nonzero(ty == BALL) + (carry[0] == BALL)
+            assert n_b == np.count_nonzero(pc[:, :, 0] == BALL) + (prev[e, p + 3] == BALL)
             unlocked = (pc[:, :, 0] == DOOR) & (pc[:, :, 2] == LOCKED) & ~((ty == DOOR) & (c[:, :, 2] == LOCKED))
             if unlocked.any():
                 assert acts[t, e] == 5 and prev[e, p + 3] == KEY
