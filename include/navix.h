@@ -126,7 +126,9 @@ NAVIX_API navix_status navix_reset(navix_env* h, uint8_t* obs, void* stream);
 
 /* reset(key) with a new key (Code 1 P:264): the handle's seed becomes
  * `seed` for this and every later level / obstacle draw, then navix_reset.
- * Equivalent to destroying the handle and creating it with `seed`. */
+ * Equivalent to destroying the handle and creating it with `seed`.
+ * Kernel arguments are passed by value: a CUDA graph captured before this
+ * call replays the old setting; recapture graphs after calling it. */
 NAVIX_API navix_status navix_reset_seed(navix_env* h, uint64_t seed, uint8_t* obs, void* stream);
 
 /* One step of every env with next-step auto-reset (R#18):
@@ -167,7 +169,9 @@ NAVIX_API navix_status navix_rollout_random(navix_env* h, uint64_t action_seed, 
  * P:673-680; R#31): every later step adds -time_cost, and
  * -action_cost unless the action is done (6), to the event reward, in binary32
  * in that order.  Auto-reset calls still return 0.  Both >= 0; 0 disables.
- * Host only, takes effect for subsequently enqueued steps. */
+ * Host only, takes effect for subsequently enqueued steps.
+ * Kernel arguments are passed by value: a CUDA graph captured before this
+ * call replays the old setting; recapture graphs after calling it. */
 NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, float action_cost);
 
 /* Reward / termination function selection (Table 6 / Table 7, P:566-589;
@@ -182,7 +186,9 @@ NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, flo
  * `free` reward function); termination_events the events that end the
  * episode (0 = `free`: only truncation ends episodes; an event that does not
  * terminate is not counted in the statistics).  Default 7 / 7 (Table 9's
- * R_1 / R_2 / R_3).  Composes with navix_set_reward_costs.  Host only. */
+ * R_1 / R_2 / R_3).  Composes with navix_set_reward_costs.  Host only.
+ * Kernel arguments are passed by value: a CUDA graph captured before this
+ * call replays the old setting; recapture graphs after calling it. */
 enum { NAVIX_EVENT_GOAL = 1, NAVIX_EVENT_LAVA = 2, NAVIX_EVENT_FAILURE = 4 };
 NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_events, uint32_t termination_events);
 
@@ -192,7 +198,9 @@ NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_e
  * alone, uint8[7][7] = 49 B (categorical_first_person) and uint8[W][H]
  * (categorical); unseen view cells are 0.  The kind applies to every obs
  * output enqueued afterwards (reset, step, step_host, rollout, observe,
- * observe_full); size obs buffers accordingly.  Host only. */
+ * observe_full); size obs buffers accordingly.  Host only.
+ * Kernel arguments are passed by value: a CUDA graph captured before this
+ * call replays the old setting; recapture graphs after calling it. */
 enum { NAVIX_OBS_SYMBOLIC = 0, NAVIX_OBS_CATEGORICAL = 1 };
 NAVIX_API navix_status navix_set_observation(navix_env* h, int kind);
 
@@ -252,6 +260,12 @@ NAVIX_API void navix_destroy(navix_env* h);
 
 /* Thread-local text of the last failure on this thread ("" if none). */
 NAVIX_API const char* navix_last_error(void);
+
+/* Build provenance: the 16-hex-digit hash of every source file and compiler
+ * flag this library was compiled from (paper_2407_19396_b200/build.py
+ * source_hash()); the tests compare it with the checked-out tree, so a stale
+ * prebuilt libnavix.so fails loudly instead of being tested.  Host only. */
+NAVIX_API const char* navix_build_id(void);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ from .navix import (  # noqa: F401
     REWARD_MINIGRID,
     REWARD_NAVIX,
     STATS_FIELDS,
+    build_id,
     NavixEnv,
     NavixError,
     load_library,

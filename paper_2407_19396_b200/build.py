@@ -2,7 +2,9 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -26,12 +28,32 @@ FLAGS = [
 ]
 
 
+def source_hash() -> str:
+    """16 hex digits of SHA-256 over every source / header this library is
+    built from and the compiler flags: the build id compiled into libnavix.so
+    (navix_build_id) and compared with the tree by the tests."""
+    h = hashlib.sha256()
+    for name in SOURCES + HEADERS:
+        h.update(name.encode() + b"\0")
+        with open(os.path.join(CSRC, name), "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def embedded_build_id(path: str = SO) -> str | None:
+    """The build id inside a built .so, read from its bytes (without loading it)."""
+    if not os.path.exists(path):
+        return None
+    with open(path, "rb") as f:
+        m = re.search(rb"NAVIX_BUILD_ID=([0-9a-f]{16})", f.read())
+    return m.group(1).decode() if m else None
+
+
 def _stale() -> bool:
-    if not os.path.exists(SO):
-        return True
-    t = os.path.getmtime(SO)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
-    return any(os.path.getmtime(d) > t for d in deps)
+    # content-addressed, not by mtime: a prebuilt .so from another tree (or a
+    # checkout that reset mtimes) is rebuilt unless its id matches this tree
+    return embedded_build_id() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -39,9 +61,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     os.makedirs(os.path.join(HERE, "..", "build"), exist_ok=True)
 
+    bid = source_hash()
+
     def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, f'-DNAVIX_BUILD_ID="{bid}"', "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(os.path.join(HERE, "..", "build", src.replace(".cu", ".ptxas.txt")), "w") as f:
             f.write(r.stderr)
@@ -65,6 +89,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc link failed")
     for o in objs:
         os.remove(o)
+    if embedded_build_id() != bid:
+        raise RuntimeError("libnavix.so does not carry the build id it was compiled with")
     return SO
 
 

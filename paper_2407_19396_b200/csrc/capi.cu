@@ -212,6 +212,13 @@ extern "C" {
 
 const char* navix_last_error(void) { return g_last_error.c_str(); }
 
+#ifndef NAVIX_BUILD_ID
+#define NAVIX_BUILD_ID "unknown0unknown0"
+#endif
+// the marker string lets build.py read the id from the .so without loading it
+__attribute__((used)) static const char k_build_id[] = "NAVIX_BUILD_ID=" NAVIX_BUILD_ID;
+const char* navix_build_id(void) { return k_build_id + 15; }
+
 navix_status navix_spec_of(const char* env_id, navix_spec* out) {
   if (!out) return fail(NAVIX_E_INVALID_ARG, "navix_spec_of: null out");
   EnvConfig c;
@@ -219,7 +226,7 @@ navix_status navix_spec_of(const char* env_id, navix_spec* out) {
   if (r == 1) return fail(NAVIX_E_UNKNOWN_ENV, "unknown env id '%s' (Table 9 ids, e.g. Navix-DoorKey-8x8-v0)",
                           env_id ? env_id : "(null)");
   fill_spec(c, out);
-  if (r == 2) return fail(NAVIX_E_UNSUPPORTED, "env id '%s' has a %dx%d grid; this build supports <= 16x16",
+  if (r == 2) return fail(NAVIX_E_UNSUPPORTED, "env id '%s' has a %dx%d grid; this build supports <= 24x24",
                           env_id, c.height, c.width);
   return NAVIX_OK;
 }
@@ -624,6 +631,9 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
   if (c.family == FAM_DYNOBS &&
       (e = cudaMemcpy(h->state + L.balls_off, balls.data(), balls.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cuda_fail(e, "import H2D balls");
+  // pageable host -> device cudaMemcpy may return before the DMA lands, and
+  // the legacy stream does not order against non-blocking streams: finish here
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
   h->initialized = true;
   return NAVIX_OK;
 }

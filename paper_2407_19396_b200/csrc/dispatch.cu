@@ -1,6 +1,7 @@
 // dispatch.cu — host-side dispatch of the step kernels (one family group per
 // translation unit, inst_*.cu) and the two small utility kernels.
 #include <cstdint>
+#include <mutex>
 
 #include "layout.h"
 #include "philox.cuh"
@@ -18,6 +19,21 @@ cudaError_t launch_group_dynobs(int, int, const KernelArgs&, int64_t, cudaStream
 cudaError_t launch_group_keycorridor(int, int, const KernelArgs&, int64_t, cudaStream_t, bool*);
 cudaError_t launch_group_lava_crossing_distshift(int, int, const KernelArgs&, int64_t, cudaStream_t, bool*);
 cudaError_t launch_group_gotodoor_fourrooms(int, int, const KernelArgs&, int64_t, cudaStream_t, bool*);
+
+// SM count of the current device (cached per device): grid-stride utility
+// kernels launch a few waves' worth of CTAs, not a hard-coded 148.
+int current_device_sm_count() {
+  constexpr int MAXD = 64;
+  static std::once_flag once[MAXD];
+  static int n_sm[MAXD];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXD) return 148;
+  std::call_once(once[dev], [dev] {
+    if (cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n_sm[dev] < 1)
+      n_sm[dev] = 148;
+  });
+  return n_sm[dev];
+}
 
 // ------------------------------------------------------------------ other kernels
 __global__ void sample_actions_kernel(uint8_t* out, int64_t n, int64_t steps, uint32_t env_begin, uint32_t t0,
@@ -61,7 +77,8 @@ __global__ void mission_kernel(const uint64_t* grid, const uint64_t* agent, int6
 cudaError_t launch_mission(const uint64_t* grid, const uint64_t* agent, int64_t n, int rw, int h, uint8_t* out,
                            cudaStream_t s) {
   int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  const int64_t cap = (int64_t)current_device_sm_count() * 16;
+  if (blocks > cap) blocks = cap;
   mission_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(grid, agent, n, rw, h, out);
   return cudaPeekAtLastError();
 }
@@ -81,7 +98,8 @@ cudaError_t launch_sample_actions(uint8_t* out, int64_t n, int64_t steps, uint32
                                   uint64_t seed, uint32_t n_actions, cudaStream_t s) {
   const int64_t total = n * steps;
   int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
+  const int64_t cap = (int64_t)current_device_sm_count() * 64;
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   sample_actions_kernel<<<(unsigned)blocks, 256, 0, s>>>(out, n, steps, env_begin, t0, (uint32_t)seed,
                                                          (uint32_t)(seed >> 32), n_actions);

@@ -27,6 +27,7 @@
 #pragma once
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "layout.h"
 #include "levelgen.cuh"
@@ -245,8 +246,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // level generator for a few lanes.  Their resetting envs are queued per CTA
   // instead and generated by the first threads (one warp for up to 32 of
   // them), each into its env's SMEM rows.
-  // (measured: the queue pays on the narrow persistent kernel, not on the
-  // 16x16 one-tile kernel, where it costs 8 % at 2^20 and 50 % at 2^16 envs)
+  // (measured with the queue on every Dynamic-Obstacles width, round-1 close:
+  // DynObs-16x16 198 -> 174 us per 2^20-env step, 14.6 -> 12.5 us at 2^16)
   constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
@@ -945,9 +946,66 @@ __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint
 }
 
 // ------------------------------------------------------------------ dispatch
+// Experiment switches (A/B measurements only), read once per process.
+inline int env_switch_onetile() {
+  static const int v = [] { const char* e = getenv("NAVIX_STEP_KERNEL"); return e && e[0] == 'o' ? 1 : 0; }();
+  return v;
+}
+inline int64_t env_switch_persist_ctas() {
+  static const int64_t v = [] { const char* e = getenv("NAVIX_PERSIST_CTAS"); return e ? (int64_t)atoll(e) : (int64_t)0; }();
+  return v;
+}
+inline int env_switch_pdl() {
+  static const int v = [] { const char* e = getenv("NAVIX_PDL"); return e && e[0] == '0' ? 0 : 1; }();
+  return v;
+}
+
 template <class K>
-inline void allow_dyn_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+inline cudaError_t allow_dyn_smem(K kernel, size_t bytes) {
+  return bytes > 48 * 1024
+             ? cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
+             : cudaSuccess;
+}
+
+// Per-device launch state of one kernel instantiation: the dynamic-SMEM
+// opt-in (cudaFuncSetAttribute applies to the current device only), the SM
+// count and the persistent kernel's occupancy.  Initialised once per device
+// under std::call_once, so several devices (and threads) in one process each
+// get their own.
+constexpr int MAX_DEVICES = 64;
+struct DeviceLaunchInfo {
+  cudaError_t err = cudaSuccess;
+  int n_sm = 0, per_sm = 0;
+};
+
+template <int FAM, int H, int W, int OBSK>
+const DeviceLaunchInfo* device_launch_info() {
+  using C = Cfg<FAM, H, W>;
+  constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL, OBSK>);
+  constexpr bool PERSIST = H * C::RW <= 16;
+  constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
+  static std::once_flag once[MAX_DEVICES];
+  static DeviceLaunchInfo info[MAX_DEVICES];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) return nullptr;
+  std::call_once(once[dev], [dev] {
+    DeviceLaunchInfo& d = info[dev];
+    cudaError_t e = cudaDeviceGetAttribute(&d.n_sm, cudaDevAttrMultiProcessorCount, dev);
+    for (cudaError_t x : {allow_dyn_smem(navix_kernel<FAM, H, W, MODE_STEP, OBSK>, DYN),
+                          allow_dyn_smem(navix_kernel<FAM, H, W, MODE_RESET, OBSK>, DYN),
+                          allow_dyn_smem(navix_kernel<FAM, H, W, MODE_OBSERVE, OBSK>, DYN),
+                          allow_dyn_smem(navix_rollout_kernel<FAM, H, W, OBSK>, DYN)})
+      if (e == cudaSuccess) e = x;
+    if constexpr (PERSIST) {
+      if (e == cudaSuccess) e = allow_dyn_smem(navix_step_persistent<FAM, H, W, OBSK>, PDYN);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE,
+                                                          PDYN);
+    }
+    if (d.per_sm < 1) d.per_sm = 1;
+    d.err = e;
+  });
+  return &info[dev];
 }
 
 template <int FAM, int H, int W, int OBSK>
@@ -955,26 +1013,16 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   const dim3 block(TILE);
   using C = Cfg<FAM, H, W>;
   constexpr size_t DYN = sizeof(OneTileSmem<FAM, C::NPL, OBSK>);
-  static bool attrs = false;
-  if (!attrs) {
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_STEP, OBSK>, DYN);
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_RESET, OBSK>, DYN);
-    allow_dyn_smem(navix_kernel<FAM, H, W, MODE_OBSERVE, OBSK>, DYN);
-    allow_dyn_smem(navix_rollout_kernel<FAM, H, W, OBSK>, DYN);
-    attrs = true;
-  }
-  static int onetile = -1;
-  if (onetile < 0) {
-    const char* v = getenv("NAVIX_STEP_KERNEL");  // experiment switch
-    onetile = v && v[0] == 'o';
-  }
+  const DeviceLaunchInfo* dl = device_launch_info<FAM, H, W, OBSK>();
+  if (!dl) return cudaErrorInvalidDevice;
+  if (dl->err != cudaSuccess) return dl->err;
   // the persistent kernel double-buffers the tile inputs in SMEM: grids up
   // to 16 row planes (8x8 and below, DistShift's 7 rows of 9); larger ones run
   // one tile per CTA, whose single buffer keeps more CTAs per SM (measured:
   // KeyCorridorS4R3 +24 %, SimpleCrossingS9N3 +11 % on the one-tile kernel)
   constexpr bool PERSIST = H * C::RW <= 16;
   constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
-  if (mode == MODE_STEP && (onetile || !PERSIST)) {
+  if (mode == MODE_STEP && (env_switch_onetile() || !PERSIST)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)n_tiles);
     cfg.blockDim = block;
@@ -988,31 +1036,12 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
     return cudaLaunchKernelEx(&cfg, navix_kernel<FAM, H, W, MODE_STEP, OBSK>, a);
   } else if (mode == MODE_STEP) {
     if constexpr (PERSIST) {
-      // persistent grid: as many CTAs as fit on the device at once
-      static int per_sm = -1, n_sm = -1;
-      if (per_sm < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        allow_dyn_smem(navix_step_persistent<FAM, H, W, OBSK>, PDYN);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, navix_step_persistent<FAM, H, W, OBSK>, TILE, PDYN);
-        if (per_sm < 1) per_sm = 1;
-      }
-      int64_t cap = (int64_t)per_sm * n_sm;
-      static int64_t ctas_env = -1;
-      if (ctas_env < 0) {
-        const char* v = getenv("NAVIX_PERSIST_CTAS");  // experiment switch: persistent grid size
-        ctas_env = v ? atoll(v) : 0;
-      }
-      if (ctas_env > 0) cap = ctas_env;
+      // persistent grid: as many CTAs as fit on this device at once
+      int64_t cap = (int64_t)dl->per_sm * dl->n_sm;
+      if (env_switch_persist_ctas() > 0) cap = env_switch_persist_ctas();
       const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
       // launched with programmatic stream serialization (PDL): back-to-back
       // steps overlap the launch of step t+1 with the tail of step t
-      static int pdl = -1;
-      if (pdl < 0) {
-        const char* v = getenv("NAVIX_PDL");
-        pdl = !(v && v[0] == '0');
-      }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = block;
@@ -1022,7 +1051,7 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
-      cfg.numAttrs = pdl ? 1 : 0;
+      cfg.numAttrs = env_switch_pdl() ? 1 : 0;
       return cudaLaunchKernelEx(&cfg, navix_step_persistent<FAM, H, W, OBSK>, a);
     }
   } else if (mode == MODE_FULL_OBS) {

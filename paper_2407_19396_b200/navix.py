@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
     "navix_set_event_functions", "navix_rollout_random", "navix_reset_seed", "navix_observe_mission", "navix_sample_actions", "navix_step_host", "navix_stats",
-    "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error",
+    "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error", "navix_build_id",
 )
 
 
@@ -93,6 +93,7 @@ def load_library():
         "navix_info": ([P, P], I32),
         "navix_destroy": ([P], None),
         "navix_last_error": ([], ctypes.c_char_p),
+        "navix_build_id": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -100,6 +101,11 @@ def load_library():
         f.restype = res
     _lib = lib
     return lib
+
+
+def build_id() -> str:
+    """Source hash libnavix.so was compiled from (see build.source_hash)."""
+    return load_library().navix_build_id().decode()
 
 
 def _check(status: int):
@@ -153,6 +159,12 @@ class NavixEnv:
         self.env_begin = int(env_begin)
         self.n_total = self.env_begin + self.n if num_envs_total is None else int(num_envs_total)
         self.seed = int(seed)
+        if state is not None:
+            need = state_bytes(env_id, self.n)
+            if (state.device != self.device or state.dtype != torch.uint8 or not state.is_contiguous()
+                    or state.numel() < need or state.data_ptr() % 256):
+                raise ValueError(f"state must be a contiguous, 256-byte aligned uint8 tensor of >= {need} bytes "
+                                 f"on {self.device}")
         self._state = state
         h = ctypes.c_void_p()
         _check(self.lib.navix_create_shard(
@@ -192,7 +204,8 @@ class NavixEnv:
         return obs
 
     def reset_seed(self, seed: int, out: torch.Tensor | None = None) -> torch.Tensor:
-        """reset(key) with a new key: every later level uses Philox key `seed`."""
+        """reset(key) with a new key: every later level uses Philox key `seed`.
+        Captured CUDA graphs keep the old key: recapture them after this call."""
         obs = self.obs if out is None else out
         self._check_out(obs, (self.n, *self.obs_shape), torch.uint8)
         self.seed = int(seed)
@@ -253,11 +266,13 @@ class NavixEnv:
         return obs, rew, term, trunc
 
     def set_reward_costs(self, time_cost: float = 0.0, action_cost: float = 0.0) -> None:
-        """Compose -time_cost per step and -action_cost per non-done action (Table 6)."""
+        """Compose -time_cost per step and -action_cost per non-done action (Table 6).
+        Captured CUDA graphs keep the old costs: recapture them after this call."""
         _check(self.lib.navix_set_reward_costs(self.h, time_cost, action_cost))
 
     def set_event_functions(self, reward_events: int = 7, termination_events: int = 7) -> None:
-        """Table 6 / 7 selection: bit 0 goal/success, 1 lava, 2 failure; 0 = `free`."""
+        """Table 6 / 7 selection: bit 0 goal/success, 1 lava, 2 failure; 0 = `free`.
+        Captured CUDA graphs keep the old selection: recapture them after this call."""
         _check(self.lib.navix_set_event_functions(self.h, reward_events, termination_events))
 
     def observe_full(self, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -302,6 +317,7 @@ class NavixEnv:
     def stats(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """Device int64[8] episode statistics of this shard (see STATS_FIELDS)."""
         o = self._stats if out is None else out
+        self._check_out(o, (8,), torch.int64)
         _check(self.lib.navix_stats(self.h, _ptr(o), _stream(self.device)))
         return o
 
