@@ -7,6 +7,11 @@ per GPU) prints ONE JSON line on rank 0:
   --envs-per-gpu envs per GPU), the HBM roofline fraction of the step kernel,
   an end-to-end number through the host-buffer C-ABI call, the CPU oracle
   timed on this host (cpu_baseline), clocks sampled during the timed region.
+`--global-envs N` splits a fixed total of N envs over the ranks instead
+(strong scaling, [CFG 5]'s 2^10..2^23 sweep); the line carries every rank's
+step time.  A steady-state (desynchronised) number is measured beside the
+synchronised one: step counts drawn uniformly over [0, T) are imported
+before a second timed region, so truncations no longer coincide.
 `--impl reference` times the CPU oracle (the reference arm of this tier) on
 rank 0 and prints its line; other ranks exit 0.
 """
@@ -182,15 +187,15 @@ def run_reference(args, rank):
     rate = calibrate_oracle(args.env)
     # bounded sample per step: the whole (warmup + steps) run within ~budget seconds
     budget = args.ref_budget_s
-    n_ref = int(max(16, min(args.envs_per_gpu, rate * budget / max(1, args.warmup + args.steps))))
+    n_ref = int(max(16, min(total_envs(args, args.gpus), rate * budget / max(1, args.warmup + args.steps))))
     value, dt = time_oracle(args.env, n_ref, args.steps, args.warmup)
     sample = (f"{n_ref} envs (global indices 0..{n_ref - 1}) of the {args.env} workload per step, "
               f"{args.steps} timed steps after {args.warmup} warm-up, single-threaded C++ oracle, {model}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": workload_config(args, args.gpus),
+        "higher_is_better": True, "scaling": "strong" if args.global_envs > 0 else "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic", "config": workload_config(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -199,11 +204,20 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def total_envs(args, world):
+    """Whole-job env count: --global-envs (strong scaling) or envs-per-GPU x ranks (weak)."""
+    return args.global_envs if args.global_envs > 0 else args.envs_per_gpu * world
+
+
 def workload_config(args, world):
+    n_total = total_envs(args, world)
+    per = (f"{args.envs_per_gpu} envs per GPU ({n_total} total)" if args.global_envs <= 0 else
+           f"{n_total} envs in total split over {world} GPU(s) (~{n_total // world} per GPU)")
     return {
-        "workload": f"{args.env}, {args.envs_per_gpu} envs per GPU ({args.envs_per_gpu * world} total), "
+        "workload": f"{args.env}, {per}, "
                     f"uniform random policy (Philox action stream), auto-reset, symbolic 7x7x3 obs",
-        "env_id": args.env, "envs_per_gpu": args.envs_per_gpu, "global_envs": args.envs_per_gpu * world,
+        "env_id": args.env, "envs_per_gpu": n_total // world if args.global_envs > 0 else args.envs_per_gpu,
+        "global_envs": n_total,
         "parallelism": f"env-sharded x{world} (NCCL all-reduce of int64[8] episode stats only)",
         "l2": "inputs larger than L2: per step per GPU ~230 MB (state 76 MB read+write, obs 154 MB) vs 126 MB L2",
         "graph": "CUDA graph of the timed steps (one step kernel launch per step)",
@@ -215,8 +229,8 @@ def run_navix(args, rank, world, local_rank):
     import torch
 
     from paper_2407_19396_b200 import NavixEnv
-    from paper_2407_19396_b200.distributed import (all_reduce_stats, init_process_group, max_over_ranks,
-                                                   mean_legacy_return, shard_for)
+    from paper_2407_19396_b200.distributed import (all_reduce_stats, gather_over_ranks, init_process_group,
+                                                   max_over_ranks, mean_legacy_return, shard_for)
 
     gpu = local_rank
     if args.backend == "gloo":  # functional test of the multi-rank path on fewer GPUs (timings meaningless)
@@ -228,7 +242,9 @@ def run_navix(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         init_process_group(args.backend, dev)
-    n_total = args.envs_per_gpu * world
+    n_total = total_envs(args, world)
+    if n_total < world:
+        raise SystemExit("--global-envs must give every rank at least one env")
     sh = shard_for(n_total, rank, world)
     begin, end, n = sh.begin, sh.end, sh.n
     env = NavixEnv(args.env, n, seed=0, env_begin=begin, num_envs_total=n_total, device=dev)
@@ -281,6 +297,7 @@ def run_navix(args, rank, world, local_rank):
     clk.mark_end()
     t_local = ev0.elapsed_time(ev1) / 1e3
     t_max = max_over_ranks(t_local, dev)
+    t_ranks = gather_over_ranks(t_local, dev)
     value = n_total * args.steps / t_max
 
     # episode statistics: the one collective of the path (NCCL all-reduce of int64[8])
@@ -362,6 +379,42 @@ def run_navix(args, rank, world, local_rank):
                        "api": "navix_step with navix_set_observation(CATEGORICAL) (row f3)"}
         del gph, cenv
 
+    # steady state: the timed region above starts right after reset, so every
+    # env's truncation falls on the same step (all episodes start together).
+    # Desynchronise them through the public state API (step counts uniform
+    # over [0, T), the parity suite's imported states), then time again.
+    steady = None
+    if args.steady_steps > 0:
+        rec = env.export_state()
+        p = 3 * spec.height * spec.width
+        rng = np.random.default_rng(1234 + rank)
+        sc = rng.integers(0, spec.max_steps, size=n).astype(np.uint16)
+        rec[:, p + 5] = (sc & 0xFF).astype(np.uint8)
+        rec[:, p + 6] = (sc >> 8).astype(np.uint8)
+        env.import_state(rec)
+        del rec
+        Ks = min(args.steady_steps, ring)
+        for t in range(args.warmup):
+            env.step(acts[t % ring])
+        torch.cuda.synchronize(dev)
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            for t in range(Ks):
+                env.step(acts[t])
+        gph.replay()
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(s)
+        gph.replay()
+        q1.record(s)
+        torch.cuda.synchronize(dev)
+        t_q = max_over_ranks(q0.elapsed_time(q1) / 1e3 / Ks, dev)
+        steady = {"steps": Ks, "value": n_total / t_q, "unit": UNIT, "ms_per_step": 1e3 * t_q,
+                  "frac_of_measured_hbm": B * n / t_q / 1e9 / measured_peaks()[0],
+                  "desync": "step counts uniform over [0, T) imported before timing (navix_state_import); "
+                            "episodes end on different steps, the steady-state auto-reset mix"}
+        del gph
+
     # end to end through the host-buffer C-ABI call (H2D actions, D2H outputs)
     h_act = torch.from_numpy(np.ascontiguousarray(acts[: args.e2e_steps].cpu().numpy())).pin_memory()
     h_obs = torch.empty((n, 7, 7, 3), dtype=torch.uint8).pin_memory()
@@ -401,7 +454,8 @@ def run_navix(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "scaling": "strong" if args.global_envs > 0 else "weak",
+        "rank_ms_per_step": [1000 * t / args.steps for t in t_ranks], "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": workload_config(args, world),
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -411,6 +465,7 @@ def run_navix(args, rank, world, local_rank):
         "gpu_launches": args.steps,
         "rollout": rollout,
         "categorical": categorical,
+        "steady_state": steady,
         "clocks": clk.summary(),
         "stats_allreduce": {"us_per_call": 1e6 * t_stats,
                             "frac_of_100_steps": t_stats / (100 * t_max / args.steps),
@@ -435,6 +490,10 @@ def main():
     ap.add_argument("--impl", default="navix", choices=["navix", "reference"])
     ap.add_argument("--env", default="DoorKey-8x8-v0")
     ap.add_argument("--envs-per-gpu", type=int, default=1 << 20)
+    ap.add_argument("--global-envs", type=int, default=0,
+                    help="fixed total env count split over the ranks (strong scaling); 0: --envs-per-gpu per rank")
+    ap.add_argument("--steady-steps", type=int, default=200,
+                    help="steps of the desynchronised steady-state measurement (0: skip)")
     ap.add_argument("--action-ring", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--rollout-steps", type=int, default=64)

@@ -610,12 +610,26 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
       const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
       cells[q & 15][q >> 4] = CELL_EMPTY;
     }
+    // Dynamic-Obstacles: agent-record flag bit 1 (layout.h) marks a static
+    // layout equal to the generator's template (walls border, goal (W-2, H-2)),
+    // which the step kernel then takes from its compile-time copy
+    uint64_t tmpl_flag = 0;
+    if (c.family == FAM_DYNOBS) {
+      bool same = true;
+      for (int y = 0; y < H && same; ++y)
+        for (int x = 0; x < W && same; ++x) {
+          const bool border = x == 0 || y == 0 || x == W - 1 || y == H - 1;
+          const uint8_t want = border ? CELL_WALL : (x == W - 2 && y == H - 2) ? CELL_GOAL : CELL_EMPTY;
+          same = cells[y][x] == want;
+        }
+      tmpl_flag = same ? 2 : 0;
+    }
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
     for (int y = 0; y < H; ++y)
       for (int x = 0; x < W; ++x)
         grid[(size_t)(tile * H * RW + y * RW + x / 8) * TILE + lane] |= (uint64_t)cells[y][x] << (8 * (x % 8));
     agent[si] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-               ((uint64_t)sc << 32) | ((uint64_t)pd << 48) | target;
+               ((uint64_t)sc << 32) | ((uint64_t)(pd | tmpl_flag) << 48) | target;
     episode[si] = ep;
     balls[si] = bl;
   }

@@ -53,6 +53,18 @@ __host__ __device__ constexpr uint64_t template_plane(int p) {
   return r;
 }
 
+// Bitboard (bit 8y + x) of the empty cells of the static layout, grids up to 8 wide.
+template <int FAM, int H, int W>
+__host__ __device__ constexpr uint64_t template_free_cells() {
+  uint64_t m = 0;
+  for (int y = 0; y < H && y < 8; ++y) {
+    const uint64_t r = template_plane<FAM, H, W>(y);
+    for (int x = 0; x < 8; ++x)
+      if (((r >> (8 * x)) & 0xFF) == CELL_EMPTY) m |= 1ull << (8 * y + x);
+  }
+  return m;
+}
+
 // Per-thread view of its env's SMEM rows: plane y * RW + x / 8 holds cells
 // x..x+7 of row y (stride TILE between planes).
 template <int RW>

@@ -199,6 +199,26 @@ __device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile
   return in;
 }
 
+// The per-CTA reset-queue counter of the Dynamic-Obstacles / GoToDoor step
+// (tile_compute).  Zero on entry: every kernel that steps those families
+// zeroes it before its first CTA barrier (init_reset_queue_counter), and
+// tile_compute zeroes it again once the queue is consumed.
+__device__ __forceinline__ int& reset_queue_counter() {
+  __shared__ int s_qn;
+  return s_qn;
+}
+// its slot list: written before the queue's first barrier, so it cannot live
+// in the tile's action staging (slower warps may still be decoding it)
+__device__ __forceinline__ uint8_t* reset_queue_slots() {
+  __shared__ uint8_t s_qslot[TILE];
+  return s_qslot;
+}
+template <int FAM>
+__device__ __forceinline__ void init_reset_queue_counter() {
+  if (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR)
+    if (threadIdx.x == 0) reset_queue_counter() = 0;
+}
+
 // a1-a6 for this thread's env: compute, then write its obs record into s_obs
 // (after before_emit() has made sure s_obs is free).  rows: this env's 8 SMEM
 // row lines (stride TILE); scratch: 8 more lines for the column view of odd
@@ -247,25 +267,31 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // instead and generated by the first threads (one warp for up to 32 of
   // them), each into its env's SMEM rows.
   // (measured with the queue on every Dynamic-Obstacles width, round-1 close:
-  // DynObs-16x16 198 -> 174 us per 2^20-env step, 14.6 -> 12.5 us at 2^16)
+  // DynObs-16x16 198 -> 174 us per 2^20-env step, 14.6 -> 12.5 us at 2^16.
+  // A warp-local queue — ballot, one generator pass per warp, no CTA barrier —
+  // measured worse, DynObs-8x8 79 -> 91 us at 2^20: four passes per tile
+  // instead of one, on an ALU-pipe-bound kernel.)
   constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
   if (COMPACT) {
-    // The queue lives in staging this tile has consumed (decoded into
-    // registers before the first barrier below): the action bytes hold the
-    // queued slots, agent record st holds (episode | generator output << 32),
-    // DynObs ball word st the new balls; no static SMEM but the counter, so
-    // the kernel keeps the occupancy of the families without a queue.
-    __shared__ int s_qn;
+    // Agent record st of the staging this tile has consumed holds (episode |
+    // generator output << 32) (each thread overwrites only the record it
+    // decoded itself), DynObs ball word st the new balls; 132 B of static
+    // SMEM for the counter and the slot list.  The counter is zero on entry
+    // (by thread 0 before the kernel's first barrier, and below after its
+    // last read), so filling the queue needs no barrier of its own.
+    int& s_qn = reset_queue_counter();
     auto* const tb = reinterpret_cast<TileSmem<FAM, C::NPL>*>(rows - tid);
-    uint8_t* const q_slot = tb->act;
+    uint8_t* const q_slot = reset_queue_slots();
     uint64_t* const q_rec = tb->agent;
     uint64_t* const q_balls = tb->balls;
-    if (tid == 0) s_qn = 0;
-    __syncthreads();
+    const unsigned rm = __ballot_sync(0xffffffffu, regen);
+    int qbase = 0;
+    if (lane == 0 && rm) qbase = atomicAdd(&s_qn, __popc(rm));  // one atomic per warp
+    qbase = __shfl_sync(0xffffffffu, qbase, 0);
     if (regen) {
-      q_slot[atomicAdd(&s_qn, 1)] = (uint8_t)tid;
+      q_slot[qbase + __popc(rm & ((1u << lane) - 1u))] = (uint8_t)tid;
       q_rec[tid] = (uint64_t)((in.episode_known ? episode : a.episode[slot]) + 1);
     }
     __syncthreads();
@@ -282,6 +308,9 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       q_rec[st] = (uint64_t)ep | ((uint64_t)out << 32);
     }
     __syncthreads();
+    // every read of the counter happened before the barrier above; the next
+    // tile's (or step's) atomics come after at least one more CTA barrier
+    if (tid == 0) s_qn = 0;
     if (regen) {
       const uint64_t qr = q_rec[tid];
       const uint32_t o = (uint32_t)(qr >> 32);
@@ -338,20 +367,89 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       grid_tmpl = FAM == FAM_DYNOBS;
     }
   }
-  if (!regen) {
-    if (FAM == FAM_DYNOBS) {
+  // Dynamic-Obstacles on grids up to 8 wide: the transition runs on 64-bit
+  // bitboards (bit 8y + x) and the balls are overlaid into the SMEM rows once,
+  // after they moved.  A warp whose envs all hold MiniGrid's static layout in
+  // HBM (agent-record flag, set by every generated level) takes the free
+  // cells from the compile-time template; a warp with an imported layout
+  // builds them from its rows.
+  constexpr bool BITBOARD = FAM == FAM_DYNOBS && RW == 1 && MODE == MODE_STEP;
+  bool warp_tmpl = false;
+  if constexpr (BITBOARD) warp_tmpl = __all_sync(0xffffffffu, grid_tmpl);
+  auto overlay_balls = [&] {
 #pragma unroll
-      for (int bb = 0; bb < C::NOBST; ++bb) {
-        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-        if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
-      }
+    for (int bb = 0; bb < C::NOBST; ++bb) {
+      const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+      if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
     }
+  };
+  if (!regen) {
+    if (FAM == FAM_DYNOBS && !BITBOARD) overlay_balls();
     if (MODE == MODE_STEP) {
       const int dx = dir == 0 ? 1 : dir == 2 ? -1 : 0;
       const int dy = dir == 1 ? 1 : dir == 3 ? -1 : 0;
       const int fx = ax + dx, fy = ay + dy;
       bool not_clear = false;
-      if (FAM == FAM_DYNOBS) {
+      if constexpr (BITBOARD) {
+        // ---- a3: transition mu (R#4, R#5, R#7) on bitboards
+        if (act >= 3) act = 0;
+        uint64_t bb_balls = 0;
+#pragma unroll
+        for (int bb = 0; bb < C::NOBST; ++bb) {
+          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+          bb_balls |= p ? 1ull << (8 * (p & 15) + (p >> 4)) : 0ull;
+        }
+        // front cell BEFORE the motion: not empty and not the goal (balls included)
+        const uint8_t f0 = g.get(fx, fy);
+        not_clear = (f0 != CELL_EMPTY && (f0 & 15) != K_GOAL) || ((bb_balls >> (8 * fy + fx)) & 1ull);
+        // admissible cells: empty in the static layout, no ball, not the agent
+        uint64_t freeb;
+        if (warp_tmpl) {
+          freeb = template_free_cells<FAM, H, W>();
+        } else {
+          freeb = 0;
+#pragma unroll
+          for (int y = 0; y < H; ++y) {
+            const uint64_t x = rows[y * TILE] ^ 0x0101010101010101ull;  // empty byte -> 0
+            const uint64_t z = ~(((x & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | x | 0x7F7F7F7F7F7F7F7Full);
+            freeb |= (((z >> 7) * 0x0102040810204080ull) >> 56) << (8 * y);  // bit x: byte x == 0
+          }
+        }
+        freeb &= ~bb_balls & ~(1ull << (8 * ay + ax));
+        const uint64_t balls_before = balls;
+        const uint4 u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
+#pragma unroll
+        for (int bb = 0; bb < C::NOBST; ++bb) {
+          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+          // the 3x3 box around an interior ball starts at bit 8 (by-1) + (bx-1) >= 0
+          const int sh = 8 * ((int)(p & 15) - 1) + ((int)(p >> 4) - 1);
+          const uint32_t w = p ? (uint32_t)(freeb >> sh) & 0x00070707u : 0u;  // row r of the box: bits 8r..8r+2
+          if (w) {
+            const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
+            uint32_t k = bounded(ub, __popc(w));  // k-th admissible cell, row-major
+            int off = 0;
+            const uint32_t c0 = __popc(w & 0xFFu), c1 = __popc(w & 0xFF00u);
+            if (k >= c0) { k -= c0; off = 8; }
+            if (k >= c1 && off == 8) { k -= c1; off = 16; }
+            uint32_t r = (w >> off) & 7u;
+            r = k >= 1 ? r & (r - 1u) : r;  // drop the lowest set bits k times (k <= 2)
+            r = k >= 2 ? r & (r - 1u) : r;
+            const int pos = sh + off + __ffs(r) - 1;
+            freeb = (freeb | (1ull << (8 * (p & 15) + (p >> 4)))) & ~(1ull << pos);  // the old cell is empty now
+            balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)(((pos & 7) << 4) | (pos >> 3)) << (8 * bb));
+          }
+        }
+        if (scratch != nullptr && balls != balls_before) {
+          // rollout: the SMEM rows persist across steps and hold last step's
+          // balls; their cells are empty in the static layout
+#pragma unroll
+          for (int bb = 0; bb < C::NOBST; ++bb) {
+            const uint32_t p = (uint32_t)(balls_before >> (8 * bb)) & 0xFF;
+            if (p) g.set(p >> 4, p & 15, CELL_EMPTY);
+          }
+        }
+        overlay_balls();
+      } else if (FAM == FAM_DYNOBS) {
         // ---- a3: transition mu (R#4, R#5, R#7)
         if (act >= 3) act = 0;
         const uint8_t f0 = g.get(fx, fy);
@@ -663,6 +761,7 @@ __global__ void __launch_bounds__(TILE, (W > 8 ? 3 : 8)) navix_kernel(const Kern
   }
   if (MODE != MODE_RESET) {
     const uint32_t mbar = smem_u32(&S.mbar);
+    if (MODE == MODE_STEP) init_reset_queue_counter<FAM>();
     if (threadIdx.x == 0) {
       mbar_init(mbar, 1);
       issue_tile_loads<FAM, H * C::RW, MODE>(a, blockIdx.x, S.buf, mbar);
@@ -761,6 +860,7 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
       t = atomicAdd(&sched[0], 1u) + 2u * gridDim.x;  // listed: already someone's
     }
   };
+  init_reset_queue_counter<FAM>();
   if (tid == 0) {
     // the first two tickets are static (b, b + grid): no burst of contended
     // atomics on the scheduler word when every CTA starts at once
@@ -829,6 +929,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   const int64_t tile = blockIdx.x, tile0 = tile * TILE, slot = tile0 + tid, e = tile0 + le;
   const bool valid = e < a.n;
   const uint32_t mbar = smem_u32(&s_mbar);
+  init_reset_queue_counter<FAM>();
   if (tid == 0) {
     mbar_init(mbar, 1);
     issue_tile_loads<FAM, H * C::RW, MODE_OBSERVE>(a, tile, s_buf, mbar);  // rows, agents (+ balls)

@@ -68,6 +68,16 @@ def max_over_ranks(x: float, device: torch.device | str = "cpu") -> float:
     return float(t.item())
 
 
+def gather_over_ranks(x: float, device: torch.device | str = "cpu") -> list[float]:
+    """Every rank's value of x, in rank order (per-rank step times)."""
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return [float(x)]
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(v.item()) for v in out]
+
+
 def mean_legacy_return(stats, max_steps: int, failure_reward: float = -1.0) -> float:
     """Mean episode return in minigrid reward mode from the reduced statistics
     (SURVEY §8c-7): (n_success - 0.9 * sum_success_step / T + failure_reward *

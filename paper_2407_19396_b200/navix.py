@@ -15,7 +15,9 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnavix.so")
+# NAVIX_LIBRARY: another build of the same ABI, for A/B measurements only (the
+# tests assert the default in-tree library matches the source tree)
+LIB_PATH = os.environ.get("NAVIX_LIBRARY") or os.path.join(_HERE, "libnavix.so")
 _lib = None
 
 NAVIX_OK, NAVIX_E_UNKNOWN_ENV, NAVIX_E_INVALID_ARG, NAVIX_E_CUDA, NAVIX_E_NOMEM, NAVIX_E_UNSUPPORTED = range(6)
