@@ -274,7 +274,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
-  if (COMPACT) {
+  // Fixed-start Dynamic-Obstacles on grids up to 8 wide (BITBOARD below):
+  // resetting lanes place their balls in the same bitboard loop that moves
+  // the other lanes' balls, so they need neither the queue nor the generator
+  constexpr bool BITBOARD = FAM == FAM_DYNOBS && RW == 1 && MODE == MODE_STEP;
+  const bool unified = BITBOARD && a.gen_param == 0;  // grid-uniform
+  if (COMPACT && !unified) {
     // Agent record st of the staging this tile has consumed holds (episode |
     // generator output << 32) (each thread overwrites only the record it
     // decoded itself), DynObs ball word st the new balls; 132 B of static
@@ -325,7 +330,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       grid_dirty = !grid_tmpl;
       grid_tmpl = FAM == FAM_DYNOBS;
     }
-  } else if (KC_WARP || regen) {
+  } else if (KC_WARP || (regen && !unified)) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
     if (MODE == MODE_STEP && regen) {
       if (!in.episode_known) episode = a.episode[slot];
@@ -370,12 +375,14 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // Dynamic-Obstacles on grids up to 8 wide: the transition runs on 64-bit
   // bitboards (bit 8y + x) and the balls are overlaid into the SMEM rows once,
   // after they moved.  A warp whose envs all hold MiniGrid's static layout in
-  // HBM (agent-record flag, set by every generated level) takes the free
-  // cells from the compile-time template; a warp with an imported layout
-  // builds them from its rows.
-  constexpr bool BITBOARD = FAM == FAM_DYNOBS && RW == 1 && MODE == MODE_STEP;
-  bool warp_tmpl = false;
-  if constexpr (BITBOARD) warp_tmpl = __all_sync(0xffffffffu, grid_tmpl);
+  // HBM (agent-record flag, set by every generated level and by imports of
+  // that layout) takes the free cells from the compile-time template; a warp
+  // with another imported layout builds them from its rows.  With a fixed
+  // start (not -Random), the lanes whose env auto-resets run the SAME loop to
+  // place their new level's balls (levelgen.cuh's DynObs generator: each ball
+  // uniform over the template's empty cells minus the agent (1,1) and the
+  // balls placed before it, draw b = word b of block (env, episode, 0, 0)):
+  // no queue, no CTA barrier, no divergent generator call.
   auto overlay_balls = [&] {
 #pragma unroll
     for (int bb = 0; bb < C::NOBST; ++bb) {
@@ -383,6 +390,87 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
     }
   };
+  bool not_clear_pre = false;  // DynObs: the front cell before the motion is not empty / goal
+  if constexpr (BITBOARD) {
+    const bool gen = unified && regen;  // this lane generates its next level here
+    const uint64_t balls_before = balls;
+    if (gen) {
+      // a2 (R#18): episode e+1 of [MG] DynamicObstaclesEnv, agent (1,1) east
+      episode = (in.episode_known ? episode : a.episode[slot]) + 1u;
+      ax = 1; ay = 1; dir = 0;
+      carry = CELL_EMPTY;
+      sc = 0;
+      prev_done = false;
+      if (!grid_tmpl) {  // an imported layout: back to the template (SMEM now, HBM at write-back)
+#pragma unroll
+        for (int y = 0; y < H; ++y) rows[y * TILE] = template_plane<FAM, H, W>(y);
+      }
+      grid_dirty = !grid_tmpl;
+      grid_tmpl = true;
+      balls = 0;
+    }
+    const bool warp_tmpl = __all_sync(0xffffffffu, grid_tmpl);
+    const bool move = !regen;
+    uint64_t bb_balls = 0;
+    if (move) {
+      if (act >= 3) act = 0;  // R#7
+#pragma unroll
+      for (int bb = 0; bb < C::NOBST; ++bb) {
+        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+        bb_balls |= p ? 1ull << (8 * (p & 15) + (p >> 4)) : 0ull;
+      }
+      const int fx = ax + (dir == 0 ? 1 : dir == 2 ? -1 : 0), fy = ay + (dir == 1 ? 1 : dir == 3 ? -1 : 0);
+      const uint8_t f0 = g.get(fx, fy);
+      not_clear_pre = (f0 != CELL_EMPTY && (f0 & 15) != K_GOAL) || ((bb_balls >> (8 * fy + fx)) & 1ull);
+    }
+    if (move || gen) {
+      // admissible cells: empty in the static layout, no ball, not the agent
+      uint64_t freeb;
+      if (warp_tmpl || gen) {
+        freeb = template_free_cells<FAM, H, W>();
+      } else {
+        freeb = 0;
+#pragma unroll
+        for (int y = 0; y < H; ++y) {
+          const uint64_t x = rows[y * TILE] ^ 0x0101010101010101ull;  // empty byte -> 0
+          const uint64_t z = ~(((x & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | x | 0x7F7F7F7F7F7F7F7Full);
+          freeb |= (((z >> 7) * 0x0102040810204080ull) >> 56) << (8 * y);  // bit x: byte x == 0
+        }
+      }
+      freeb &= ~bb_balls & ~(1ull << (8 * ay + ax));
+      // generation: (env, episode, 0, block 0); transition: (env, episode, 1 << 16 | step, 0)
+      const uint4 u = philox4x32_10(make_uint4(genv, episode, gen ? 0u : (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
+      uint32_t fails = 0;
+#pragma unroll
+      for (int bb = 0; bb < C::NOBST; ++bb) {
+        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+        // transition: the 3x3 box around the ball (interior: starts at bit
+        // 8 (by-1) + (bx-1) >= 0); generation: every free cell
+        const int sh = 8 * ((int)(p & 15) - 1) + ((int)(p >> 4) - 1);
+        const uint64_t m = gen ? freeb : p ? freeb & (0x070707ull << sh) : 0ull;
+        if (m) {
+          const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
+          const int pos = select64(m, bounded(ub, __popcll(m)));  // k-th admissible cell, row-major
+          const uint64_t old = gen ? 0ull : 1ull << (8 * (p & 15) + (p >> 4));  // empty now
+          freeb = (freeb | old) & ~(1ull << pos);
+          balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)(((pos & 7) << 4) | (pos >> 3)) << (8 * bb));
+        } else {
+          fails += gen ? 1u : 0u;  // [MG] place_obj would raise; the ball is left out (stats)
+        }
+      }
+      if (gen) st_fail = fails;
+      if (scratch != nullptr && balls != balls_before) {
+        // rollout: the SMEM rows persist across steps and hold last step's
+        // balls; their cells are empty in the static layout
+#pragma unroll
+        for (int bb = 0; bb < C::NOBST; ++bb) {
+          const uint32_t p = (uint32_t)(balls_before >> (8 * bb)) & 0xFF;
+          if (p) g.set(p >> 4, p & 15, CELL_EMPTY);
+        }
+      }
+    }
+    if (!regen || gen) overlay_balls();  // (queue-generated levels already hold theirs)
+  }
   if (!regen) {
     if (FAM == FAM_DYNOBS && !BITBOARD) overlay_balls();
     if (MODE == MODE_STEP) {
@@ -391,64 +479,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       const int fx = ax + dx, fy = ay + dy;
       bool not_clear = false;
       if constexpr (BITBOARD) {
-        // ---- a3: transition mu (R#4, R#5, R#7) on bitboards
-        if (act >= 3) act = 0;
-        uint64_t bb_balls = 0;
-#pragma unroll
-        for (int bb = 0; bb < C::NOBST; ++bb) {
-          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-          bb_balls |= p ? 1ull << (8 * (p & 15) + (p >> 4)) : 0ull;
-        }
-        // front cell BEFORE the motion: not empty and not the goal (balls included)
-        const uint8_t f0 = g.get(fx, fy);
-        not_clear = (f0 != CELL_EMPTY && (f0 & 15) != K_GOAL) || ((bb_balls >> (8 * fy + fx)) & 1ull);
-        // admissible cells: empty in the static layout, no ball, not the agent
-        uint64_t freeb;
-        if (warp_tmpl) {
-          freeb = template_free_cells<FAM, H, W>();
-        } else {
-          freeb = 0;
-#pragma unroll
-          for (int y = 0; y < H; ++y) {
-            const uint64_t x = rows[y * TILE] ^ 0x0101010101010101ull;  // empty byte -> 0
-            const uint64_t z = ~(((x & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | x | 0x7F7F7F7F7F7F7F7Full);
-            freeb |= (((z >> 7) * 0x0102040810204080ull) >> 56) << (8 * y);  // bit x: byte x == 0
-          }
-        }
-        freeb &= ~bb_balls & ~(1ull << (8 * ay + ax));
-        const uint64_t balls_before = balls;
-        const uint4 u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
-#pragma unroll
-        for (int bb = 0; bb < C::NOBST; ++bb) {
-          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-          // the 3x3 box around an interior ball starts at bit 8 (by-1) + (bx-1) >= 0
-          const int sh = 8 * ((int)(p & 15) - 1) + ((int)(p >> 4) - 1);
-          const uint32_t w = p ? (uint32_t)(freeb >> sh) & 0x00070707u : 0u;  // row r of the box: bits 8r..8r+2
-          if (w) {
-            const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
-            uint32_t k = bounded(ub, __popc(w));  // k-th admissible cell, row-major
-            int off = 0;
-            const uint32_t c0 = __popc(w & 0xFFu), c1 = __popc(w & 0xFF00u);
-            if (k >= c0) { k -= c0; off = 8; }
-            if (k >= c1 && off == 8) { k -= c1; off = 16; }
-            uint32_t r = (w >> off) & 7u;
-            r = k >= 1 ? r & (r - 1u) : r;  // drop the lowest set bits k times (k <= 2)
-            r = k >= 2 ? r & (r - 1u) : r;
-            const int pos = sh + off + __ffs(r) - 1;
-            freeb = (freeb | (1ull << (8 * (p & 15) + (p >> 4)))) & ~(1ull << pos);  // the old cell is empty now
-            balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)(((pos & 7) << 4) | (pos >> 3)) << (8 * bb));
-          }
-        }
-        if (scratch != nullptr && balls != balls_before) {
-          // rollout: the SMEM rows persist across steps and hold last step's
-          // balls; their cells are empty in the static layout
-#pragma unroll
-          for (int bb = 0; bb < C::NOBST; ++bb) {
-            const uint32_t p = (uint32_t)(balls_before >> (8 * bb)) & 0xFF;
-            if (p) g.set(p >> 4, p & 15, CELL_EMPTY);
-          }
-        }
-        overlay_balls();
+        not_clear = not_clear_pre;  // a3 ran above
       } else if (FAM == FAM_DYNOBS) {
         // ---- a3: transition mu (R#4, R#5, R#7)
         if (act >= 3) act = 0;

@@ -55,9 +55,23 @@ CATALOG = ["Empty-5x5-v0", "Empty-6x6-v0", "Empty-8x8-v0", "Empty-16x16-v0", "Em
 CATALOG_SIZES = [1 << 11, 1 << 16, 1 << 20]
 
 
-def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5):
+def desynchronise(env, seed: int = 1234):
+    """Steady state: step counts uniform over [0, T) through the public state
+    API, so the episodes no longer all truncate on the same step."""
+    rec = env.export_state()
+    s = env.spec
+    p = 3 * s.height * s.width
+    sc = np.random.default_rng(seed).integers(0, s.max_steps, size=env.n).astype(np.uint16)
+    rec[:, p + 5] = (sc & 0xFF).astype(np.uint8)
+    rec[:, p + 6] = (sc >> 8).astype(np.uint8)
+    env.import_state(rec)
+
+
+def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5, desync: bool = False):
     env = NavixEnv(env_id, n, seed=0)
     env.reset()
+    if desync:
+        desynchronise(env)
     ring = min(steps, 256)
     acts = env.sample_actions(1, 0, ring)
     for t in range(warmup):
@@ -92,7 +106,7 @@ def time_point(env_id: str, n: int, steps: int, warmup: int = 10, runs: int = 5)
             "GBps": B * n / t / 1e9, "frac_of_measured_hbm": B * n / t / 1e9 / peak, "bytes_per_env_step": B,
             # the layout's bytes: grid rows padded to 8-byte planes (layout.h)
             "padded_bytes_per_env_step": Bp, "frac_of_measured_hbm_padded": Bp * n / t / 1e9 / peak,
-            "episodes": st[0]}
+            "episodes": st[0], "desync": desync}
 
 
 def time_rollout(env_id: str, n: int, K: int, runs: int = 5):
@@ -128,6 +142,8 @@ def main():
     ap.add_argument("--runs", type=int, default=5, help="timed repetitions per point (percentiles)")
     ap.add_argument("--catalog", action="store_true", help="every Table 9 id at 2^11 / 2^16 / 2^20 envs")
     ap.add_argument("--rollout-k", type=int, default=0, help="time navix_rollout_random with K steps per launch")
+    ap.add_argument("--desync", action="store_true",
+                    help="steady state: desynchronise the episodes' step counts before timing")
     a = ap.parse_args()
     rows = []
     sizes = [int(x) for x in a.sizes.split(",") if x] or SIZES
@@ -146,7 +162,7 @@ def main():
                     continue
                 r = time_rollout(env_id, n, a.rollout_k, runs=a.runs)
             else:
-                r = time_point(env_id, n, a.steps, runs=a.runs)
+                r = time_point(env_id, n, a.steps, runs=a.runs, desync=a.desync)
             rows.append(r)
             pad = r.get("frac_of_measured_hbm_padded")
             print(f"{env_id:28s} N={n:>8d}  {r['us_per_step']:9.2f} us/step  {r['env_steps_per_s'] / 1e9:8.3f} G/s  "
