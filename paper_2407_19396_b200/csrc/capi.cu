@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,6 +26,16 @@ cudaError_t launch_mission(const uint64_t* grid, const uint64_t* agent, int64_t 
 
 using namespace navix;
 
+// Steps of at most this many envs run the small-batch kernel (navix_step_wide,
+// DESIGN.md §6.5).  NAVIX_WIDE_MAX overrides the default (A/B measurements).
+static int64_t default_wide_max() {
+  static const int64_t v = [] {
+    const char* e = getenv("NAVIX_WIDE_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)NAVIX_DEFAULT_WIDE_MAX;
+  }();
+  return v;
+}
+
 struct navix_env {
   EnvConfig cfg;
   navix_spec spec;
@@ -37,6 +48,7 @@ struct navix_env {
   bool initialized = false;  // a reset or an import has written the state
   uint32_t reward_events = 7, termination_events = 7;  // navix_set_event_functions (R#42)
   float time_cost = 0.f, action_cost = 0.f;
+  int64_t wide_max = default_wide_max();  // navix_set_small_batch_threshold
   uint8_t* state;
   bool owns_state;
   // navix_step_host staging (lazily allocated)
@@ -166,6 +178,7 @@ KernelArgs make_args(navix_env* h) {
   a.obs_kind = h->obs_kind;
   a.reward_events = h->reward_events;
   a.termination_events = h->termination_events;
+  a.wide_max = h->wide_max;
   return a;
 }
 
@@ -390,6 +403,13 @@ navix_status navix_set_event_functions(navix_env* h, uint32_t reward_events, uin
     return fail(NAVIX_E_INVALID_ARG, "event masks use bits 0-2 only (got %#x, %#x)", reward_events, termination_events);
   h->reward_events = reward_events;
   h->termination_events = termination_events;
+  return NAVIX_OK;
+}
+
+navix_status navix_set_small_batch_threshold(navix_env* h, int64_t max_envs) {
+  if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_small_batch_threshold: null handle");
+  if (max_envs < 0) return fail(NAVIX_E_INVALID_ARG, "threshold must be >= 0 (0 disables the small-batch kernel)");
+  h->wide_max = max_envs;
   return NAVIX_OK;
 }
 

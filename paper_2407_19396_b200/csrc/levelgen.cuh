@@ -5,6 +5,7 @@
 // (global env, episode, 0, block); rejection loops replaced by one uniform
 // draw over the admissible set in row-major order; connect_all keeps its loop.
 #pragma once
+#include <type_traits>
 #include "layout.h"
 #include "philox.cuh"
 
@@ -139,6 +140,96 @@ __device__ __forceinline__ uint32_t pick8(const uint4& x0, const uint4& x1, uint
   return u == 0 ? x.x : u == 1 ? x.y : u == 2 ? x.z : x.w;
 }
 
+// The draws of one level, cached across a warp that generates it together
+// (generate_level<..., WARP = true>): lane l holds Philox block base + l of
+// the stream (env, episode, 0, block), so 128 consecutive draws cost ONE
+// parallel Philox evaluation instead of 32 sequential ones, and any draw is a
+// shuffle away.  Same draws as DrawStream, in the same order.
+struct WarpDraws {
+  uint32_t c0, c1, k0, k1;
+  uint32_t base;  // block held by lane 0
+  uint32_t pos;   // next draw index (DrawStream::pos)
+  uint4 blk;      // this lane's block: base + lane
+  __device__ WarpDraws(uint32_t env, uint32_t episode, uint32_t key_lo, uint32_t key_hi)
+      : c0(env), c1(episode), k0(key_lo), k1(key_hi), base(0), pos(0) {
+    refill(0);
+  }
+  __device__ __forceinline__ void refill(uint32_t b) {  // warp-uniform b
+    base = b;
+    blk = philox4x32_10(make_uint4(c0, c1, 0u, b + (threadIdx.x & 31)), k0, k1);
+  }
+  // block b (cached: b - base < 32, warp-uniform or not) from its lane
+  __device__ __forceinline__ uint4 block(uint32_t b) const {
+    const int src = (int)(b - base);
+    return make_uint4(__shfl_sync(0xffffffffu, blk.x, src), __shfl_sync(0xffffffffu, blk.y, src),
+                      __shfl_sync(0xffffffffu, blk.z, src), __shfl_sync(0xffffffffu, blk.w, src));
+  }
+  // make blocks [b, b + n) resident (warp-uniform b, n <= 32)
+  __device__ __forceinline__ void ensure(uint32_t b, uint32_t n) {
+    if (b < base || b + n > base + 32u) refill(b);
+  }
+  __device__ __forceinline__ uint32_t next() {  // warp-uniform
+    const uint32_t k = pos++;
+    ensure(k >> 2, 1);
+    const uint32_t t = k & 3;
+    const uint32_t mine = t == 0 ? blk.x : t == 1 ? blk.y : t == 2 ? blk.z : blk.w;
+    return __shfl_sync(0xffffffffu, mine, (int)((k >> 2) - base));
+  }
+  __device__ __forceinline__ uint32_t next_bounded(uint32_t n) { return bounded(next(), n); }
+};
+
+// A generator with a fixed draw sequence (no data-dependent branch around a
+// draw): its NB Philox blocks are computed up front, independent of each
+// other (instruction-level parallelism instead of NB chained evaluations),
+// and every draw's block and word are compile-time constants after inlining.
+template <int NB>
+struct FixedDraws {
+  uint4 b[NB];
+  uint32_t pos;
+  __device__ FixedDraws(uint32_t env, uint32_t episode, uint32_t klo, uint32_t khi) : pos(0) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) b[i] = philox4x32_10(make_uint4(env, episode, 0u, (uint32_t)i), klo, khi);
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const uint32_t k = pos++;
+    const uint4& x = b[k >> 2];
+    const uint32_t t = k & 3;
+    return t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;
+  }
+  __device__ __forceinline__ uint32_t next_bounded(uint32_t n) { return bounded(next(), n); }
+};
+
+// The draw source of generate_level: one thread's DrawStream, the warp's
+// cache (KeyCorridor generated by a whole warp), or the prefetched blocks of
+// a fixed draw sequence (GoToDoor 13 draws, DoorKey 5, FourRooms 7).
+template <int FAM, bool WARP>
+struct LevelDrawsT {
+  using type = DrawStream;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_KEYCORRIDOR, WARP> {
+  using type = typename std::conditional<WARP, WarpDraws, DrawStream>::type;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_GOTODOOR, WARP> {
+  using type = FixedDraws<4>;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_DOORKEY, WARP> {
+  using type = FixedDraws<2>;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_FOURROOMS, WARP> {
+  using type = FixedDraws<2>;
+};
+__device__ __forceinline__ DrawStream make_draws(DrawStream*, uint32_t env, uint32_t ep, uint32_t klo, uint32_t khi) {
+  return DrawStream(env, ep, 0u, klo, khi);
+}
+template <class D>
+__device__ __forceinline__ D make_draws(D*, uint32_t env, uint32_t ep, uint32_t klo, uint32_t khi) {
+  return D(env, ep, klo, khi);
+}
+
 // WARP: the whole warp calls this for ONE env (same arguments in every lane,
 // converged) and KeyCorridor's connect_all runs 32 of its iterations at once
 // (see the loop); every other family and step is computed redundantly.
@@ -152,7 +243,8 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
   __builtin_assume(__isShared(g.rows));
 #pragma unroll
   for (int p = 0; p < H * C::RW; ++p) g.rows[p * TILE] = template_plane<FAM, H, W>(p);
-  DrawStream ds(genv, episode, 0u, klo, khi);
+  using Draws = typename LevelDrawsT<FAM, WARP>::type;
+  Draws ds = make_draws(static_cast<Draws*>(nullptr), genv, episode, klo, khi);
 
   if constexpr (FAM == FAM_EMPTY_RANDOM) {
     // [MG] EmptyEnv with agent_start_pos=None: place_agent() over the empty
@@ -468,9 +560,10 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       for (;;) {
         if (it > 5000) { o.fail += 1; break; }
         if (reach == all) break;
+        ds.ensure(p >> 2, ((p + 3u * 31u) >> 2) + 2u - (p >> 2));  // this round's <= 26 blocks
         const uint32_t q = p + 3u * lane, b0 = q >> 2, t0 = q & 3;
-        const uint4 x0 = philox4x32_10(make_uint4(genv, episode, 0u, b0), klo, khi);
-        const uint4 x1 = philox4x32_10(make_uint4(genv, episode, 0u, b0 + 1u), klo, khi);
+        const uint4 x0 = ds.block(b0);
+        const uint4 x1 = ds.block(b0 + 1u);
         const int i = (int)bounded(pick8(x0, x1, t0), NC);
         const int j = (int)bounded(pick8(x0, x1, t0 + 1), NR);
         const int k = (int)bounded(pick8(x0, x1, t0 + 2), 4);

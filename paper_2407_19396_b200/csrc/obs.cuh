@@ -295,15 +295,10 @@ __device__ __forceinline__ void view_oob_walls(int ax, int ay, int dir, uint32_t
 // process_vis of the 7x7 view (byte vj of vis_lo / vis_hi has bit vi set iff
 // view cell (vi, vj) is visible; bit 7 of each byte is garbage — the callers
 // only ever move bit vi, vi <= 6, to a sign position).
-__device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const uint32_t (&chi)[7], uint32_t& vis_lo,
-                                                uint32_t& vis_hi) {
-  // opacity rows: byte vj of op has bit vi set iff cell (vi, vj) is opaque
-  uint32_t op_lo = 0, op_hi = 0;
-#pragma unroll
-  for (int vi = 0; vi < 7; ++vi) {
-    op_lo |= (clo[vi] >> (7 - vi)) & (0x01010101u << vi);
-    op_hi |= (chi[vi] >> (7 - vi)) & (0x01010101u << vi);
-  }
+// process_vis from the opacity rows: byte vj of op_lo (vj 0..3) / op_hi
+// (vj 4..6) has bit vi set iff view cell (vi, vj) is opaque.
+__device__ __forceinline__ void visibility_closure(uint32_t op_lo, uint32_t op_hi, uint32_t& vis_lo,
+                                                   uint32_t& vis_hi) {
   // transparency rows and their 7-bit reversals (bit vi -> bit 6-vi)
   const uint32_t t_lo = ~op_lo & 0x7F7F7F7Fu, t_hi = ~op_hi & 0x7F7F7F7Fu;
   const uint32_t tr_lo = (prmt(__brev(t_lo), 0u, 0x0123u) >> 1) & 0x7F7F7F7Fu;
@@ -338,6 +333,18 @@ __device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const 
   }
 }
 
+__device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const uint32_t (&chi)[7], uint32_t& vis_lo,
+                                                uint32_t& vis_hi) {
+  // opacity rows: byte vj of op has bit vi set iff cell (vi, vj) is opaque
+  uint32_t op_lo = 0, op_hi = 0;
+#pragma unroll
+  for (int vi = 0; vi < 7; ++vi) {
+    op_lo |= (clo[vi] >> (7 - vi)) & (0x01010101u << vi);
+    op_hi |= (chi[vi] >> (7 - vi)) & (0x01010101u << vi);
+  }
+  visibility_closure(op_lo, op_hi, vis_lo, vis_hi);
+}
+
 // Everything after the view columns: opacity, process_vis, encode, emission.
 // out: word-aligned SMEM address at or before this env's record, whose first
 // byte is at misalignment M (warp-uniform, 0..3).  All 7 columns are encoded
@@ -362,6 +369,52 @@ __device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)
     case 2: emit_record<2>(out, r); break;
     default: emit_record<3>(out, r); break;
   }
+}
+
+// ---------------------------------------------------------------- one column
+// The small-batch kernel (navix_step_wide) splits one env's observation over
+// lanes: lane vi builds view column vi only.  Grids up to 8 wide; `rows` are
+// the env's 8 SMEM row lines (stride TILE).  Even directions read one world
+// row (as view_columns_narrow); odd ones gather the world column byte by byte
+// (no in-place transpose: the rows are shared by the env's lanes).
+__device__ __forceinline__ void view_column_narrow(const uint64_t* rows, int ax, int ay, int dir, int vi,
+                                                   uint32_t& clo, uint32_t& chi) {
+  const int base = dir == 0 ? ay - 3 : dir == 1 ? ax + 3 : dir == 2 ? ay + 3 : ax - 3;
+  const int sgn = (dir == 0 || dir == 3) ? 1 : -1;
+  const int s = (dir == 0 ? ax : dir == 1 ? ay : dir == 2 ? ax - 6 : ay - 6) & 7;
+  const bool rev = dir <= 1;
+  const uint32_t s4 = (uint32_t)s * 0x1111u;
+  const uint32_t sel_lo = (s4 + (rev ? 0x3456u : 0x3210u)) & 0x7777u;
+  const uint32_t sel_hi = (s4 + (rev ? 0x0012u : 0x7654u)) & 0x7777u;
+  const int li = (base + sgn * vi) & 7;
+  uint32_t lo, hi;
+  if ((dir & 1) == 0) {
+    const uint64_t line = rows[li * TILE];
+    lo = (uint32_t)line;
+    hi = (uint32_t)(line >> 32);
+  } else {  // world column li: byte y = cell (li, y)
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(rows) + li;
+    constexpr int R = TILE * 8;  // bytes between row lines
+    lo = prmt(prmt(b[0], b[R], 0x0040u), prmt(b[2 * R], b[3 * R], 0x0040u), 0x5410u);
+    hi = prmt(prmt(b[4 * R], b[5 * R], 0x0040u), prmt(b[6 * R], b[7 * R], 0x0040u), 0x5410u);
+  }
+  clo = prmt(lo, hi, sel_lo);
+  chi = prmt(lo, hi, sel_hi);
+}
+
+// The 21 record bytes of one encoded column (encode_col's registers r[0..5])
+// in stream order (t c s per cell vj), stored byte by byte at dst.
+__device__ __forceinline__ void store_column_bytes(uint8_t* dst, const uint32_t (&r)[7]) {
+  // r0 = t0 c0 t1 c1, r1 = t2 c2 t3 c3, r2 = s0 s1 s2 s3, r3 = t4 c4 t5 c5, r4 = t6 c6 . ., r5 = s4 s5 s6 .
+  const uint32_t w0 = prmt(r[0], r[2], 0x2410u);                      // t0 c0 s0 t1
+  const uint32_t w1 = prmt(prmt(r[0], r[2], 0x0053u), r[1], 0x5410u);  // c1 s1 t2 c2
+  const uint32_t w2 = prmt(r[1], r[2], 0x7326u);                      // s2 t3 c3 s3
+  const uint32_t w3 = prmt(r[3], r[5], 0x2410u);                      // t4 c4 s4 t5
+  const uint32_t w4 = prmt(prmt(r[3], r[5], 0x0053u), r[4], 0x5410u);  // c5 s5 t6 c6
+  const uint32_t w[5] = {w0, w1, w2, w3, w4};
+#pragma unroll
+  for (int k = 0; k < 20; ++k) dst[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+  dst[20] = (uint8_t)(r[5] >> 16);                                    // s6
 }
 
 // ---------------------------------------------------------------- categorical

@@ -224,13 +224,23 @@ __device__ __forceinline__ void init_reset_queue_counter() {
 // row lines (stride TILE); scratch: 8 more lines for the column view of odd
 // directions, or nullptr to transpose the rows in place (then the rows are
 // written back to HBM first if the grid changed, and are lost).
-template <int FAM, int H, int W, int MODE, int OBSK, class BeforeEmit>
+//
+// WIDE (navix_step_wide, small batches): WIDE_LANES consecutive lanes share
+// one env, tile-local env `wide_le`, and all compute its step redundantly on
+// the same inputs (their SMEM writes are identical); there is no CTA queue or
+// warp-cooperative generator, the grid write-back is split over the lanes,
+// and the function returns before the observation, which the lanes split by
+// view column (navix_step_wide).
+constexpr int WIDE_LANES = 8;
+template <int FAM, int H, int W, int MODE, int OBSK, class BeforeEmit, bool WIDE = false>
 __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t tile, uint64_t* rows, uint64_t* scratch,
-                                                  const EnvIn& in, uint8_t* s_obs, BeforeEmit before_emit) {
+                                                  const EnvIn& in, uint8_t* s_obs, BeforeEmit before_emit,
+                                                  int wide_le = 0) {
   using C = Cfg<FAM, H, W>;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int le = 4 * lane + warp;
+  // state slot and env of this thread within the tile (layout.h: slot 32 w + l <-> env 4 l + w)
+  const int tid = WIDE ? slot_of_env(wide_le) : (int)threadIdx.x;
+  const int warp = tid >> 5, lane = WIDE ? (int)(threadIdx.x & 31) : tid & 31;
+  const int le = WIDE ? wide_le : 4 * lane + warp;
   const int64_t tile0 = tile * TILE;
   const int64_t slot = tile0 + tid;   // state index
   const int64_t e = tile0 + le;       // env index (caller arrays)
@@ -271,8 +281,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // A warp-local queue — ballot, one generator pass per warp, no CTA barrier —
   // measured worse, DynObs-8x8 79 -> 91 us at 2^20: four passes per tile
   // instead of one, on an ALU-pipe-bound kernel.)
-  constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP;
-  constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP;
+  constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP && !WIDE;
+  constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP && !WIDE;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
   // Fixed-start Dynamic-Obstacles on grids up to 8 wide (BITBOARD below):
   // resetting lanes place their balls in the same bitboard loop that moves
@@ -555,7 +565,11 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       const bool f_out = FAM == FAM_GOTODOOR && ((unsigned)fx >= (unsigned)W || (unsigned)fy >= (unsigned)H);
       const uint32_t fc = f_out ? (uint32_t)CELL_WALL : *fp;
       const uint32_t kind = fc & 15u;
-      const bool is_fwd = act == 2, is_pick = act == 3, is_drop = act == 4, is_tog = act == 5;
+      // (Dynamic-Obstacles maps every action >= 3 to left, R#7: no pickup,
+      // drop or toggle can happen, and the compiler drops their logic)
+      constexpr bool MANIP = FAM != FAM_DYNOBS;
+      const bool is_fwd = act == 2, is_pick = MANIP && act == 3, is_drop = MANIP && act == 4,
+                 is_tog = MANIP && act == 5;
       dir = (dir + (act == 1 ? 1 : 0) + (act == 0 ? 3 : 0)) & 3;
       const bool walk = (0x31Au >> kind) & 1u;  // empty, floor, open door, goal, lava
       ax = (is_fwd && walk) ? fx : ax;
@@ -630,13 +644,34 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // one 32-byte sector instead of H*RW of them)
   if (MODE != MODE_OBSERVE && grid_dirty && scratch == nullptr) {
     uint64_t* gdst = a.grid + tile0 * H * RW + tid;
+    const int wl = (int)(threadIdx.x % WIDE_LANES);  // WIDE: lane wl writes planes p = wl mod WIDE_LANES
     if (FAM != FAM_DYNOBS && dirty_plane >= 0) {
-      gdst[dirty_plane * TILE] = rows[dirty_plane * TILE];
+      if (!WIDE || wl == 0) gdst[dirty_plane * TILE] = rows[dirty_plane * TILE];
     } else {
 #pragma unroll
       for (int p = 0; p < H * RW; ++p)
-        gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : rows[p * TILE];
+        if (!WIDE || p % WIDE_LANES == wl)
+          gdst[p * TILE] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(p) : rows[p * TILE];
     }
+  }
+  if constexpr (WIDE) {  // the observation is split over the lanes by the caller
+    EnvResult r;
+    r.reward = reward;
+    r.valid = valid;
+    r.regen = regen;
+    r.term = term;
+    r.trunc = trunc;
+    r.dirty = grid_dirty;
+    r.tvalid = false;
+    r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) |
+             ((uint64_t)carry << 24) | ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) |
+             ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)target << 56);
+    r.episode = episode;
+    r.balls = balls;
+    const uint32_t vv = valid && (threadIdx.x % WIDE_LANES) == 0 ? 1u : 0u;  // counted once per env
+    r.st[0] = st_ep * vv; r.st[1] = st_len * vv; r.st[2] = st_succ * vv; r.st[3] = st_succ_len * vv;
+    r.st[4] = st_lava * vv; r.st[5] = st_coll * vv; r.st[6] = st_trunc * vv; r.st[7] = st_fail * vv;
+    return r;
   }
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
@@ -856,7 +891,12 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
   // small batches (<= 4 tiles per CTA): plain striding, no scheduler atomics
   // on the critical path; larger ones balance with the atomic counter
   constexpr bool RESET_FIRST_FAM = FAM == FAM_KEYCORRIDOR;
-  const bool stride_only = n_tiles <= 4 * (int64_t)gridDim.x;
+  // KeyCorridor keeps the dynamic scheduler whenever a CTA gets more than one
+  // tile: in steady state (desynchronised episodes, ~1/270 of the envs reset
+  // every step) a third of the tiles carry a long level generation, and
+  // claiming those first balances them over the CTAs (striding stacked up to
+  // four of them on one CTA)
+  const bool stride_only = n_tiles <= (RESET_FIRST_FAM ? 1 : 4) * (int64_t)gridDim.x;
   if (tid == 0) {
     mbar_init(smem_u32(&s_mbar[0]), 1);
     mbar_init(smem_u32(&s_mbar[1]), 1);
@@ -941,6 +981,115 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
       }
     }
   }
+}
+
+// Small batches (SURVEY §8d's 2^10-2^14 points, the paper's 2048 agents
+// P:43): one step of n envs is a handful of tiles, so its time is one env's
+// dependent chain, not bandwidth.  Here WIDE_LANES lanes
+// share an env: they run its step logic redundantly (tile_compute<WIDE>),
+// split the grid write-back, and each builds ONE view column of the
+// observation (the visibility rows are OR-reduced over the lanes with
+// shuffles), so the observation's ~500 dependent instructions become ~100.
+// 16 envs per 128-thread CTA; records staged in SMEM and copied out by their
+// warp with word stores.  Grids up to 8 wide with a closed border (not
+// GoToDoor).  Bit-identical to navix_step_persistent (tests/test_gpu_wide.py).
+constexpr int WIDE_EPC = TILE / WIDE_LANES;  // envs per CTA
+struct NoEmit {
+  __device__ void operator()() const {}
+};
+template <int FAM, int H, int W, int OBSK>
+__global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
+  using C = Cfg<FAM, H, W>;
+  static_assert(C::RW == 1, "the small-batch kernel covers grids up to 8 wide");
+  constexpr int OB = obs_record_bytes(OBSK);
+  __shared__ __align__(16) uint64_t s_rows[8][TILE];  // env g's lines in column g (stride TILE, as RowViewT)
+  __shared__ __align__(16) uint8_t s_obs[WIDE_EPC * OB];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = threadIdx.x, g = t / WIDE_LANES, j = t % WIDE_LANES;
+  const int64_t e = (int64_t)blockIdx.x * WIDE_EPC + g;
+  const bool valid = e < a.n;
+  const int64_t tile = e / TILE;
+  const int le = (int)(e % TILE), st = slot_of_env(le);
+  const int64_t slot = tile * TILE + st;
+  uint64_t* const rows = &s_rows[0][g];
+  // inputs: lane j loads grid row j; every lane the agent record (one
+  // broadcast transaction per env); padding envs get a legal dummy state
+  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, FAM == FAM_DYNOBS, false};
+  if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
+  if (valid) {
+    in.rec = a.agent[slot];
+    in.act = a.actions[e];
+    if (FAM == FAM_DYNOBS) {
+      in.balls = a.balls[slot];
+      in.episode = a.episode[slot];
+    }
+  }
+  __syncwarp();
+  const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(a, tile, rows, nullptr, in, nullptr,
+                                                                          NoEmit{}, le);
+  __syncwarp();
+  // ---- a6 split by view column: lane j < 7 builds column vi = j
+  const int ax = (int)(r.nrec & 0xFF), ay = (int)((r.nrec >> 8) & 0xFF), dir = (int)((r.nrec >> 16) & 3);
+  const uint32_t carry = (uint32_t)((r.nrec >> 24) & 0xFF);
+  uint32_t clo = 0, chi = 0;
+  if (j < 7) view_column_narrow(rows, ax, ay, dir, j, clo, chi);
+  const int js = j < 7 ? j : 0;
+  uint32_t op_lo = j < 7 ? (clo >> (7 - js)) & (0x01010101u << js) : 0u;  // byte vj, bit vi: opaque
+  uint32_t op_hi = j < 7 ? (chi >> (7 - js)) & (0x01010101u << js) : 0u;
+#pragma unroll
+  for (int k = 1; k < WIDE_LANES; k <<= 1) {  // OR over the env's lanes (aligned groups of 8)
+    op_lo |= __shfl_xor_sync(0xffffffffu, op_lo, k);
+    op_hi |= __shfl_xor_sync(0xffffffffu, op_hi, k);
+  }
+  uint32_t vis_lo, vis_hi;
+  visibility_closure(op_lo, op_hi, vis_lo, vis_hi);
+  if (j == 3) chi = prmt(chi, carry, 0x3410u);  // the agent sees what it carries (R#13)
+  if (j < 7) {
+    const uint32_t m_lo = prmt(vis_lo * (1u << (7 - js)), 0u, 0xBA98u);
+    const uint32_t m_hi = prmt(vis_hi * (1u << (7 - js)), 0u, 0xBA98u);
+    if constexpr (OBSK == OBS_CATEGORICAL) {
+      const uint32_t tl = encode4_type(clo, m_lo), th = encode4_type(chi, m_hi);
+      uint8_t* d = s_obs + g * OB + 7 * j;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[k] = (uint8_t)(tl >> (8 * k));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d[4 + k] = (uint8_t)(th >> (8 * k));
+    } else {
+      uint32_t rr[7];
+      encode_col(clo, chi, m_lo, m_hi, 0u, rr);
+      store_column_bytes(s_obs + g * OB + 21 * j, rr);
+    }
+  }
+  __syncwarp();
+  // ---- a7: each warp copies its 4 envs' records (contiguous, 4-byte aligned)
+  {
+    const int w = t >> 5, l = t & 31;
+    const int64_t e0 = (int64_t)blockIdx.x * WIDE_EPC + 4 * w;
+    const int64_t nv = a.n - e0;
+    const int nbytes = (int)(nv <= 0 ? 0 : nv >= 4 ? 4 * OB : nv * OB);
+    const uint8_t* src = s_obs + 4 * w * OB;
+    uint8_t* dst = a.obs + e0 * OB;
+    if ((reinterpret_cast<uintptr_t>(dst) & 3u) == 0) {
+      const int nw = nbytes >> 2;
+      for (int i = l; i < nw; i += 32)
+        reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+      for (int i = 4 * nw + l; i < nbytes; i += 32) dst[i] = src[i];
+    } else {
+      for (int i = l; i < nbytes; i += 32) dst[i] = src[i];
+    }
+  }
+  if (valid && j == 0) {
+    a.reward[e] = r.reward;
+    a.terminated[e] = r.term;
+    a.truncated[e] = r.trunc;
+    a.agent[slot] = r.nrec;
+    if (r.regen) a.episode[slot] = r.episode;
+    if (FAM == FAM_DYNOBS) a.balls[slot] = r.balls;
+  }
+  StatsAcc acc;
+  acc.add(r);
+  acc.flush(a);
 }
 
 // f1: K consecutive steps of one tile in one CTA.  The grid rows
@@ -1154,6 +1303,22 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   // KeyCorridorS4R3 +24 %, SimpleCrossingS9N3 +11 % on the one-tile kernel)
   constexpr bool PERSIST = H * C::RW <= 16;
   constexpr size_t PDYN = sizeof(PersistSmem<FAM, C::NPL, OBSK>);
+  // small batches: the multi-lane-per-env kernel (navix_step_wide)
+  constexpr bool WIDE_OK = C::RW == 1 && FAM != FAM_GOTODOOR;
+  if constexpr (WIDE_OK) {
+    if (mode == MODE_STEP && a.n <= a.wide_max) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((a.n + WIDE_EPC - 1) / WIDE_EPC));
+      cfg.blockDim = block;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, navix_step_wide<FAM, H, W, OBSK>, a);
+    }
+  }
   if (mode == MODE_STEP && (env_switch_onetile() || !PERSIST)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)n_tiles);

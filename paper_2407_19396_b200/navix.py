@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "navix_spec_of", "navix_state_bytes", "navix_create", "navix_create_shard", "navix_reset",
     "navix_step", "navix_rollout", "navix_observe", "navix_observe_full", "navix_set_reward_costs", "navix_set_observation",
     "navix_set_event_functions", "navix_rollout_random", "navix_reset_seed", "navix_observe_mission", "navix_sample_actions", "navix_step_host", "navix_stats",
-    "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error", "navix_build_id",
+    "navix_state_export", "navix_state_import", "navix_info", "navix_destroy", "navix_last_error", "navix_build_id", "navix_set_small_batch_threshold",
 )
 
 
@@ -96,8 +96,11 @@ def load_library():
         "navix_destroy": ([P], None),
         "navix_last_error": ([], ctypes.c_char_p),
         "navix_build_id": ([], ctypes.c_char_p),
+        "navix_set_small_batch_threshold": ([P, I64], I32),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("NAVIX_LIBRARY") and not hasattr(lib, name):
+            continue  # A/B against an older build: its missing entry points stay unbound
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
@@ -271,6 +274,11 @@ class NavixEnv:
         """Compose -time_cost per step and -action_cost per non-done action (Table 6).
         Captured CUDA graphs keep the old costs: recapture them after this call."""
         _check(self.lib.navix_set_reward_costs(self.h, time_cost, action_cost))
+
+    def set_small_batch_threshold(self, max_envs: int) -> None:
+        """Steps of at most max_envs envs use the multi-lane-per-env kernel (0: never).
+        Bit-identical results; captured CUDA graphs keep the old choice."""
+        _check(self.lib.navix_set_small_batch_threshold(self.h, int(max_envs)))
 
     def set_event_functions(self, reward_events: int = 7, termination_events: int = 7) -> None:
         """Table 6 / 7 selection: bit 0 goal/success, 1 lava, 2 failure; 0 = `free`.
