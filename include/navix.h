@@ -192,13 +192,15 @@ NAVIX_API navix_status navix_set_reward_costs(navix_env* h, float time_cost, flo
 enum { NAVIX_EVENT_GOAL = 1, NAVIX_EVENT_LAVA = 2, NAVIX_EVENT_FAILURE = 4 };
 NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_events, uint32_t termination_events);
 
-/* Small batches: a step of at most max_envs envs runs the
- * multi-lane-per-env kernel (8 lanes share an env and split its observation
- * by view column), larger ones the persistent one-thread-per-env kernel.
- * Results are bit-identical either way; only the latency differs.  Default
- * NAVIX_DEFAULT_WIDE_MAX (512; environment variable NAVIX_WIDE_MAX
- * overrides it per process); 0 disables.  Grids up to 8 wide except
- * GoToDoor.  Host only; graphs captured earlier keep the old choice. */
+/* Small batches: a step or rollout of at most max_envs envs
+ * runs the multi-lane-per-env kernels (8 lanes share an env and split its
+ * observation by view column), larger ones the one-thread-per-env kernels.
+ * Results are bit-identical either way; only the latency differs.  Defaults:
+ * 512 envs for steps (NAVIX_DEFAULT_WIDE_MAX, environment variable
+ * NAVIX_WIDE_MAX) and 4096 for rollouts (NAVIX_DEFAULT_WIDE_MAX_ROLLOUT,
+ * NAVIX_WIDE_MAX_ROLLOUT); this call sets both; 0 disables.  Grids up to 8
+ * wide except GoToDoor.  Host only; graphs captured earlier keep the old
+ * choice. */
 NAVIX_API navix_status navix_set_small_batch_threshold(navix_env* h, int64_t max_envs);
 
 /* Observation kinds (Table 5; R#41).  SYMBOLIC (the

@@ -26,13 +26,19 @@ cudaError_t launch_mission(const uint64_t* grid, const uint64_t* agent, int64_t 
 
 using namespace navix;
 
-// Steps of at most this many envs run the small-batch kernel (navix_step_wide,
-// DESIGN.md §6.5).  NAVIX_WIDE_MAX overrides the default (A/B measurements).
+// Steps (rollouts) of at most this many envs run the small-batch kernels
+// (navix_step_wide / navix_rollout_wide).  NAVIX_WIDE_MAX /
+// NAVIX_WIDE_MAX_ROLLOUT override the defaults (A/B measurements).
+static int64_t env_or(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return e ? (int64_t)atoll(e) : dflt;
+}
 static int64_t default_wide_max() {
-  static const int64_t v = [] {
-    const char* e = getenv("NAVIX_WIDE_MAX");
-    return e ? (int64_t)atoll(e) : (int64_t)NAVIX_DEFAULT_WIDE_MAX;
-  }();
+  static const int64_t v = env_or("NAVIX_WIDE_MAX", NAVIX_DEFAULT_WIDE_MAX);
+  return v;
+}
+static int64_t default_wide_max_rollout() {
+  static const int64_t v = env_or("NAVIX_WIDE_MAX_ROLLOUT", NAVIX_DEFAULT_WIDE_MAX_ROLLOUT);
   return v;
 }
 
@@ -49,6 +55,7 @@ struct navix_env {
   uint32_t reward_events = 7, termination_events = 7;  // navix_set_event_functions (R#42)
   float time_cost = 0.f, action_cost = 0.f;
   int64_t wide_max = default_wide_max();  // navix_set_small_batch_threshold
+  int64_t wide_max_rollout = default_wide_max_rollout();
   uint8_t* state;
   bool owns_state;
   // navix_step_host staging (lazily allocated)
@@ -179,6 +186,7 @@ KernelArgs make_args(navix_env* h) {
   a.reward_events = h->reward_events;
   a.termination_events = h->termination_events;
   a.wide_max = h->wide_max;
+  a.wide_max_rollout = h->wide_max_rollout;
   return a;
 }
 
@@ -410,6 +418,7 @@ navix_status navix_set_small_batch_threshold(navix_env* h, int64_t max_envs) {
   if (!h) return fail(NAVIX_E_INVALID_ARG, "navix_set_small_batch_threshold: null handle");
   if (max_envs < 0) return fail(NAVIX_E_INVALID_ARG, "threshold must be >= 0 (0 disables the small-batch kernel)");
   h->wide_max = max_envs;
+  h->wide_max_rollout = max_envs;
   return NAVIX_OK;
 }
 

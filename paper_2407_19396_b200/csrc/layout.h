@@ -35,6 +35,9 @@ constexpr int TILE = 128;   // envs per CTA (one thread per env)
 #ifndef NAVIX_DEFAULT_WIDE_MAX
 #define NAVIX_DEFAULT_WIDE_MAX 512  // small-batch kernel up to this many envs (measured)
 #endif
+#ifndef NAVIX_DEFAULT_WIDE_MAX_ROLLOUT
+#define NAVIX_DEFAULT_WIDE_MAX_ROLLOUT 4096  // the same for rollouts (measured)
+#endif
 constexpr int NSLOT = 512;  // stats stripes (atomics spread over 512 x 64 B)
 constexpr int OBS_BYTES = 147;
 // Observation kinds (Table 5, R#41): the first-person record is
@@ -143,6 +146,7 @@ struct KernelArgs {
   // navix_sample_actions stream (key act_key, counter (env, act_t0 + t, 2 << 16, 0))
   uint32_t act_key_lo, act_key_hi, act_t0;
   int64_t wide_max;     // steps of at most this many envs run navix_step_wide (small batches)
+  int64_t wide_max_rollout;  // rollouts of at most this many envs run navix_rollout_wide
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };

@@ -994,41 +994,17 @@ __global__ void __launch_bounds__(TILE) navix_step_persistent(const KernelArgs a
 // warp with word stores.  Grids up to 8 wide with a closed border (not
 // GoToDoor).  Bit-identical to navix_step_persistent (tests/test_gpu_wide.py).
 constexpr int WIDE_EPC = TILE / WIDE_LANES;  // envs per CTA
-struct NoEmit {
-  __device__ void operator()() const {}
-};
-template <int FAM, int H, int W, int OBSK>
-__global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
-  using C = Cfg<FAM, H, W>;
-  static_assert(C::RW == 1, "the small-batch kernel covers grids up to 8 wide");
+// a6 + a7 of the small-batch kernels: lane j < 7 of an env builds view
+// column vi = j of its observation (after the step in r), the visibility rows
+// are OR-reduced over the env's lanes, each lane writes its column's record
+// bytes to SMEM, and each warp copies its 4 envs' records (contiguous,
+// 4-byte aligned) to a.obs.  Called by all lanes of the CTA, converged.
+template <int OBSK>
+__device__ __forceinline__ void wide_observe_and_store(const KernelArgs& a, const EnvResult& r, const uint64_t* rows,
+                                                       uint8_t* s_obs) {
   constexpr int OB = obs_record_bytes(OBSK);
-  __shared__ __align__(16) uint64_t s_rows[8][TILE];  // env g's lines in column g (stride TILE, as RowViewT)
-  __shared__ __align__(16) uint8_t s_obs[WIDE_EPC * OB];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int t = threadIdx.x, g = t / WIDE_LANES, j = t % WIDE_LANES;
-  const int64_t e = (int64_t)blockIdx.x * WIDE_EPC + g;
-  const bool valid = e < a.n;
-  const int64_t tile = e / TILE;
-  const int le = (int)(e % TILE), st = slot_of_env(le);
-  const int64_t slot = tile * TILE + st;
-  uint64_t* const rows = &s_rows[0][g];
-  // inputs: lane j loads grid row j; every lane the agent record (one
-  // broadcast transaction per env); padding envs get a legal dummy state
-  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, FAM == FAM_DYNOBS, false};
-  if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
-  if (valid) {
-    in.rec = a.agent[slot];
-    in.act = a.actions[e];
-    if (FAM == FAM_DYNOBS) {
-      in.balls = a.balls[slot];
-      in.episode = a.episode[slot];
-    }
-  }
-  __syncwarp();
-  const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(a, tile, rows, nullptr, in, nullptr,
-                                                                          NoEmit{}, le);
-  __syncwarp();
+  __syncwarp();  // the warp's previous copy-out (rollout) has read s_obs
   // ---- a6 split by view column: lane j < 7 builds column vi = j
   const int ax = (int)(r.nrec & 0xFF), ay = (int)((r.nrec >> 8) & 0xFF), dir = (int)((r.nrec >> 16) & 3);
   const uint32_t carry = (uint32_t)((r.nrec >> 24) & 0xFF);
@@ -1079,6 +1055,45 @@ __global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
       for (int i = l; i < nbytes; i += 32) dst[i] = src[i];
     }
   }
+}
+
+
+struct NoEmit {
+  __device__ void operator()() const {}
+};
+template <int FAM, int H, int W, int OBSK>
+__global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
+  using C = Cfg<FAM, H, W>;
+  static_assert(C::RW == 1, "the small-batch kernel covers grids up to 8 wide");
+  constexpr int OB = obs_record_bytes(OBSK);
+  __shared__ __align__(16) uint64_t s_rows[8][TILE];  // env g's lines in column g (stride TILE, as RowViewT)
+  __shared__ __align__(16) uint8_t s_obs[WIDE_EPC * OB];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = threadIdx.x, g = t / WIDE_LANES, j = t % WIDE_LANES;
+  const int64_t e = (int64_t)blockIdx.x * WIDE_EPC + g;
+  const bool valid = e < a.n;
+  const int64_t tile = e / TILE;
+  const int le = (int)(e % TILE), st = slot_of_env(le);
+  const int64_t slot = tile * TILE + st;
+  uint64_t* const rows = &s_rows[0][g];
+  // inputs: lane j loads grid row j; every lane the agent record (one
+  // broadcast transaction per env); padding envs get a legal dummy state
+  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, FAM == FAM_DYNOBS, false};
+  if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
+  if (valid) {
+    in.rec = a.agent[slot];
+    in.act = a.actions[e];
+    if (FAM == FAM_DYNOBS) {
+      in.balls = a.balls[slot];
+      in.episode = a.episode[slot];
+    }
+  }
+  __syncwarp();
+  const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(a, tile, rows, nullptr, in, nullptr,
+                                                                          NoEmit{}, le);
+  __syncwarp();
+  wide_observe_and_store<OBSK>(a, r, rows, s_obs);
   if (valid && j == 0) {
     a.reward[e] = r.reward;
     a.terminated[e] = r.term;
@@ -1089,6 +1104,77 @@ __global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
   }
   StatsAcc acc;
   acc.add(r);
+  acc.flush(a);
+}
+
+// f1 at small batches: K steps of 16 envs per CTA with 8 lanes per env (as
+// navix_step_wide), the rows in SMEM and the agent record / episode / balls
+// in registers across the K steps; bit-identical to K navix_step calls.
+template <int FAM, int H, int W, int OBSK>
+__global__ void __launch_bounds__(TILE) navix_rollout_wide(const KernelArgs a, int64_t K) {
+  using C = Cfg<FAM, H, W>;
+  static_assert(C::RW == 1, "the small-batch kernel covers grids up to 8 wide");
+  constexpr int OB = obs_record_bytes(OBSK);
+  __shared__ __align__(16) uint64_t s_rows[8][TILE];
+  __shared__ __align__(16) uint8_t s_obs[WIDE_EPC * OB];
+  const int t = threadIdx.x, g = t / WIDE_LANES, j = t % WIDE_LANES;
+  const int64_t e = (int64_t)blockIdx.x * WIDE_EPC + g;
+  const bool valid = e < a.n;
+  const int64_t tile = e / TILE;
+  const int le = (int)(e % TILE), st = slot_of_env(le);
+  const int64_t slot = tile * TILE + st;
+  uint64_t* const rows = &s_rows[0][g];
+  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, true, false};
+  if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
+  if (valid) {
+    in.rec = a.agent[slot];
+    in.episode = a.episode[slot];
+    if (FAM == FAM_DYNOBS) in.balls = a.balls[slot];
+  }
+  const bool draw = a.actions == nullptr;  // in-kernel random policy (navix_rollout_random)
+  const uint32_t genv = a.env_begin + (uint32_t)e;
+  auto policy = [&](int64_t tt) -> uint32_t {
+    const uint4 w = philox4x32_10(make_uint4(genv, a.act_t0 + (uint32_t)tt, 2u << 16, 0u), a.act_key_lo, a.act_key_hi);
+    return bounded(w.x, (uint32_t)C::NA);
+  };
+  uint32_t next_act = !valid ? 0u : draw ? policy(0) : a.actions[e];
+  bool dirty = false;
+  StatsAcc acc;
+  __syncwarp();
+  for (int64_t k = 0; k < K; ++k) {
+    in.act = next_act;
+    if (k + 1 < K && valid) next_act = draw ? policy(k + 1) : a.actions[(k + 1) * a.n + e];  // one step ahead
+    KernelArgs as = a;
+    as.obs = a.obs + k * a.n * OB;
+    as.reward = a.reward + k * a.n;
+    as.terminated = a.terminated + k * a.n;
+    as.truncated = a.truncated + k * a.n;
+    // a non-null scratch: the rows stay in SMEM (no per-step grid write-back;
+    // Dynamic-Obstacles clears its balls' old cells there)
+    const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(
+        as, tile, rows, reinterpret_cast<uint64_t*>(s_obs), in, nullptr, NoEmit{}, le);
+    __syncwarp();
+    wide_observe_and_store<OBSK>(as, r, rows, s_obs);
+    if (valid && j == 0) {
+      as.reward[e] = r.reward;
+      as.terminated[e] = r.term;
+      as.truncated[e] = r.trunc;
+    }
+    acc.add(r);
+    in.rec = r.nrec;
+    in.episode = r.episode;
+    in.balls = r.balls;
+    dirty |= r.dirty;
+  }
+  if (valid) {
+    if (j == 0) {
+      a.agent[slot] = in.rec;
+      a.episode[slot] = in.episode;
+      if (FAM == FAM_DYNOBS) a.balls[slot] = in.balls;
+    }
+    if (dirty && j < H)
+      a.grid[(tile * H + j) * TILE + st] = FAM == FAM_DYNOBS ? template_plane<FAM, H, W>(j) : rows[j * TILE];
+  }
   acc.flush(a);
 }
 
@@ -1354,6 +1440,13 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   } else if (mode == MODE_FULL_OBS) {
     full_obs_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
   } else if (mode == MODE_ROLLOUT) {
+    if constexpr (WIDE_OK) {
+      if (a.n <= a.wide_max_rollout) {
+        navix_rollout_wide<FAM, H, W, OBSK><<<(unsigned)((a.n + WIDE_EPC - 1) / WIDE_EPC), block, 0, s>>>(
+            a, a.rollout_steps);
+        return cudaPeekAtLastError();
+      }
+    }
     navix_rollout_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a, a.rollout_steps);
   } else if (mode == MODE_RESET) {
     navix_kernel<FAM, H, W, MODE_RESET, OBSK><<<(unsigned)n_tiles, block, DYN, s>>>(a);

@@ -18,10 +18,16 @@ pytestmark = pytest.mark.gpu
     ("Empty-Random-6x6-v0", 300, 150), ("DistShift1-v0", 300, 120),
     ("SimpleCrossingS9N3-v0", 300, 150), ("GoToDoor-8x8-v0", 300, 100),
     ("FourRooms-v0", 300, 130)])
-def test_rollout_equals_sequential_steps(env_id, n, K):
+@pytest.mark.parametrize("small_batch_kernels", [True, False])
+def test_rollout_equals_sequential_steps(env_id, n, K, small_batch_kernels):
+    # small_batch_kernels=False: the one-tile-per-CTA rollout and the
+    # persistent step at every size (navix_set_small_batch_threshold(0))
     from paper_2407_19396_b200 import NavixEnv
     a = NavixEnv(env_id, n, seed=8)
     b = NavixEnv(env_id, n, seed=8)
+    if not small_batch_kernels:
+        a.set_small_batch_threshold(0)
+        b.set_small_batch_threshold(0)
     a.reset()
     b.reset()
     acts = torch.from_numpy(random_actions(6, 2 * K, n, 0, high=8)).cuda()

@@ -96,3 +96,54 @@ def test_wide_and_persistent_kernels_interleave(env_id):
         g.set_small_batch_threshold(1 << 30 if k % 2 == 0 else 0)
         _step_all(g, o, acts[30 * k:30 * (k + 1)])
     np.testing.assert_array_equal(g.export_state(), o.export())
+
+
+@pytest.mark.parametrize("env_id", IDS)
+@pytest.mark.parametrize("n,K", [(17, 120), (333, 60)])
+def test_wide_rollout_vs_oracle(env_id, n, K):
+    # navix_rollout_wide: the state stays in SMEM / registers across K steps
+    from paper_2407_19396_b200 import NavixEnv
+    g = NavixEnv(env_id, n, seed=13)
+    g.set_small_batch_threshold(1 << 30)
+    o = OracleEnv(env_id, n, seed=13)
+    g.reset()
+    o.reset()
+    acts = random_actions(9, 2 * K, n, 0, high=8)
+    for half in range(2):  # two launches: the state is carried over in HBM
+        ro, rr, rte, rtr = g.rollout(torch.from_numpy(acts[half * K:(half + 1) * K]).cuda())
+        for t in range(K):
+            oo, orw, ote, otr = o.step(acts[half * K + t])
+            np.testing.assert_array_equal(ro[t].cpu().numpy(), oo, err_msg=f"rollout obs {half} {t}")
+            np.testing.assert_array_equal(rr[t].cpu().numpy().view(np.uint32), orw.view(np.uint32))
+            np.testing.assert_array_equal(rte[t].cpu().numpy(), ote)
+            np.testing.assert_array_equal(rtr[t].cpu().numpy(), otr)
+        np.testing.assert_array_equal(g.export_state(), o.export())
+    np.testing.assert_array_equal(g.stats().cpu().numpy(), o.stats())
+
+
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "Dynamic-Obstacles-8x8-v0", "KeyCorridorS3R3-v0"])
+def test_wide_rollout_random_categorical_and_tile_kernel(env_id):
+    # the in-kernel policy and categorical obs on the small-batch rollout, and
+    # the one-tile-per-CTA rollout kernel forced at the same size: all equal
+    from paper_2407_19396_b200 import NavixEnv
+    from oracle import sample_actions as oracle_sample_actions
+    n, K = 300, 50
+    a = NavixEnv(env_id, n, seed=3, observation="categorical")
+    b = NavixEnv(env_id, n, seed=3, observation="categorical")
+    a.set_small_batch_threshold(1 << 30)
+    b.set_small_batch_threshold(0)
+    o = OracleEnv(env_id, n, seed=3)
+    a.reset()
+    b.reset()
+    o.reset()
+    ra = a.rollout_random(21, 4, K)
+    rb = b.rollout_random(21, 4, K)
+    for x, y in zip(ra, rb):
+        assert torch.equal(x, y)
+    acts = oracle_sample_actions(21, 0, n, 4, K, o.spec.n_actions)
+    for t in range(K):
+        oo, orw, ote, otr = o.step(acts[t])
+        np.testing.assert_array_equal(ra[0][t].cpu().numpy(), oo[..., 0])
+        np.testing.assert_array_equal(ra[1][t].cpu().numpy().view(np.uint32), orw.view(np.uint32))
+    np.testing.assert_array_equal(a.export_state(), o.export())
+    np.testing.assert_array_equal(b.export_state(), o.export())
