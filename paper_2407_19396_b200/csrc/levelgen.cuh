@@ -480,18 +480,32 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     Hl |= 1u << (locked_room - 1);
     // object placement inside room (ri, rj): empty, not the default agent
     // cell, Manhattan distance >= 2 from it (reject_next_to, R#25)
+    // WARP (the whole warp builds this level): lane l evaluates candidate
+    // cell l of a room and ballots assemble the mask, instead of every lane
+    // walking all S*S cells (rooms of up to 32 cells)
+    constexpr bool LANES = WARP && S * S <= 32;
+    const int lane = (int)(threadIdx.x & 31);
     auto place_in_room = [&](int ri, int rj, uint8_t cell) {
       const uint32_t u = ds.next();
       uint64_t m = 0;
       int n = 0;
-      for (int yy = 0; yy < S; ++yy)
-        for (int xx = 0; xx < S; ++xx) {
-          const int x = ri * (S - 1) + xx, y = rj * (S - 1) + yy;
-          const int d = abs(x - adx) + abs(y - ady);
-          const bool ok = x < W && y < H && g.get(x, y) == CELL_EMPTY && d >= 2;
-          m |= (ok ? 1ull : 0ull) << (yy * S + xx);
-          n += ok;
-        }
+      if (LANES) {
+        const int xx = lane % S, yy = lane / S;
+        const int x = ri * (S - 1) + xx, y = rj * (S - 1) + yy;
+        const bool ok = lane < S * S && x < W && y < H && g.get(x < W ? x : 0, y < H ? y : 0) == CELL_EMPTY &&
+                        abs(x - adx) + abs(y - ady) >= 2;
+        m = __ballot_sync(0xffffffffu, ok);
+        n = __popc((uint32_t)m);
+      } else {
+        for (int yy = 0; yy < S; ++yy)
+          for (int xx = 0; xx < S; ++xx) {
+            const int x = ri * (S - 1) + xx, y = rj * (S - 1) + yy;
+            const int d = abs(x - adx) + abs(y - ady);
+            const bool ok = x < W && y < H && g.get(x, y) == CELL_EMPTY && d >= 2;
+            m |= (ok ? 1ull : 0ull) << (yy * S + xx);
+            n += ok;
+          }
+      }
       if (n == 0) { o.fail += 1; return; }
       const int p = select64(m, bounded(u, (uint32_t)n));
       g.set(ri * (S - 1) + p % S, rj * (S - 1) + p / S, cell);
@@ -509,6 +523,39 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       for (int w = 0; w < NWD; ++w) m[w] = 0;
       int n = 0;
       const int rx = S - 1, ry = (NR / 2) * (S - 1);
+      if (LANES) {
+        // lane c holds candidate cell c's 4 directions as a nibble; the k-th
+        // candidate (row-major, direction innermost) is found by prefix counts
+        const int xx = lane % S, yy = lane / S, x = rx + xx, y = ry + yy;
+        uint32_t nib = 0;
+        if (lane < S * S && g.get(x, y) == CELL_EMPTY) {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const uint8_t f = g.get(x + (d == 0) - (d == 2), y + (d == 1) - (d == 3));
+            nib |= (f == CELL_EMPTY || (f & 15) == K_WALL) ? 1u << d : 0u;
+          }
+        }
+        const uint32_t cnt = __popc(nib);
+        uint32_t excl = 0;  // candidates in lanes below this one
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+          excl += __popc(__ballot_sync(0xffffffffu, (nib >> d) & 1u) & ((1u << lane) - 1u));
+        const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+        if (total == 0) {
+          o.fail += 1;
+        } else {
+          const uint32_t k = bounded(u, total);
+          const int owner = __ffs(__ballot_sync(0xffffffffu, excl <= k && k < excl + cnt)) - 1;
+          uint32_t r = __shfl_sync(0xffffffffu, nib, owner);
+          const uint32_t kk = k - __shfl_sync(0xffffffffu, excl, owner);  // kk-th set bit of r (kk <= 3)
+          r = kk >= 1 ? r & (r - 1u) : r;
+          r = kk >= 2 ? r & (r - 1u) : r;
+          r = kk >= 3 ? r & (r - 1u) : r;
+          o.dir = __ffs(r) - 1;
+          o.ax = rx + owner % S;
+          o.ay = ry + owner / S;
+        }
+      } else {
       for (int yy = 0; yy < S; ++yy)
         for (int xx = 0; xx < S; ++xx) {
           const int x = rx + xx, y = ry + yy;
@@ -533,6 +580,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
         o.dir = p & 3;
         o.ax = rx + (p >> 2) % S;
         o.ay = ry + (p >> 2) / S;
+      }
       }
     }
     // connect_all(max_itrs = 5000): reachability from the agent's room is kept
