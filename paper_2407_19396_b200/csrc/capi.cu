@@ -227,6 +227,22 @@ void from_cell(uint8_t c, uint8_t* t) {
 
 bool walkable_kind(uint8_t kind) { return (0x31Au >> kind) & 1u; }
 
+// levelgen.cuh STATIC_LAYOUT / template_plane, for the run-time config of a handle
+bool static_layout_family(int f) {
+  return f == FAM_DYNOBS || f == FAM_EMPTY || f == FAM_EMPTY_RANDOM || f == FAM_DISTSHIFT1 || f == FAM_DISTSHIFT2;
+}
+uint8_t template_cell(const EnvConfig& c, int x, int y) {
+  const int W = c.width, H = c.height;
+  if (x == 0 || y == 0 || x == W - 1 || y == H - 1) return CELL_WALL;
+  if (c.family == FAM_DISTSHIFT1 || c.family == FAM_DISTSHIFT2) {  // R#33
+    const int strip2 = c.family == FAM_DISTSHIFT1 ? 2 : 5;
+    if (x == W - 2 && y == 1) return CELL_GOAL;
+    if (x >= 3 && x < W - 3 && (y == 1 || y == strip2)) return CELL_LAVA;
+    return CELL_EMPTY;
+  }
+  return (x == W - 2 && y == H - 2) ? CELL_GOAL : CELL_EMPTY;
+}
+
 }  // namespace
 
 extern "C" {
@@ -308,10 +324,18 @@ navix_status navix_create_shard(const char* env_id, int64_t num_envs_total, int6
   {  // scheduler and statistics start at zero even before the first reset
     DeviceGuard dg(device);
     e = cudaMemset(h->state + h->layout.stats_off, 0, h->layout.total - h->layout.stats_off);
+    if (e == cudaSuccess && static_layout_family(h->cfg.family)) {
+      // the per-device visibility table of the static-layout families
+      // (step_kernel.cuh obs_table_kernel); idempotent, outside any capture
+      KernelArgs a{};
+      a.obs_kind = OBS_SYMBOLIC;
+      e = launch_env_kernel(h->cfg, MODE_OBS_TABLE, a, 1, nullptr);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
     if (e != cudaSuccess) {
       if (h->owns_state) cudaFree(h->state);
       delete h;
-      return cuda_fail(e, "cudaMemset(stats)");
+      return cuda_fail(e, "cudaMemset(stats) / observation table");
     }
   }
   *out = h;
@@ -639,18 +663,14 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
       const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
       cells[q & 15][q >> 4] = CELL_EMPTY;
     }
-    // Dynamic-Obstacles: agent-record flag bit 1 (layout.h) marks a static
-    // layout equal to the generator's template (walls border, goal (W-2, H-2)),
-    // which the step kernel then takes from its compile-time copy
+    // static-layout families: agent-record flag bit 1 (layout.h) marks a
+    // layout equal to the generator's template (levelgen.cuh template_plane),
+    // which the step kernel then knows without reading it
     uint64_t tmpl_flag = 0;
-    if (c.family == FAM_DYNOBS) {
+    if (static_layout_family(c.family)) {
       bool same = true;
       for (int y = 0; y < H && same; ++y)
-        for (int x = 0; x < W && same; ++x) {
-          const bool border = x == 0 || y == 0 || x == W - 1 || y == H - 1;
-          const uint8_t want = border ? CELL_WALL : (x == W - 2 && y == H - 2) ? CELL_GOAL : CELL_EMPTY;
-          same = cells[y][x] == want;
-        }
+        for (int x = 0; x < W && same; ++x) same = cells[y][x] == template_cell(c, x, y);
       tmpl_flag = same ? 2 : 0;
     }
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;

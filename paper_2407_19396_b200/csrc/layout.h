@@ -149,6 +149,7 @@ struct KernelArgs {
   int64_t wide_max_rollout;  // rollouts of at most this many envs run navix_rollout_wide
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4 };
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_ROLLOUT = 3, MODE_FULL_OBS = 4,
+                  MODE_OBS_TABLE = 5 /* build the Dynamic-Obstacles observation table (step_kernel.cuh) */ };
 
 }  // namespace navix

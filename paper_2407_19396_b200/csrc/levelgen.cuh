@@ -26,6 +26,12 @@ struct Cfg {
   static constexpr int NOBST = FAM != FAM_DYNOBS ? 0 : (W == 5 ? 2 : W == 6 ? 3 : W == 16 ? 8 : 4);  // R#6
 };
 
+// Families whose every level has the same layout (template_plane below):
+// only the agent and, in Dynamic-Obstacles, the see-through balls differ.
+template <int FAM>
+constexpr bool STATIC_LAYOUT = FAM == FAM_DYNOBS || FAM == FAM_EMPTY || FAM == FAM_EMPTY_RANDOM ||
+                               FAM == FAM_DISTSHIFT1 || FAM == FAM_DISTSHIFT2;
+
 // Static layout plane p (row y = p / RW, cells x = 8 (p % RW) .. +7) as 8
 // cell bytes (cells x >= W are 0 = outside the grid).
 template <int FAM, int H, int W>

@@ -345,15 +345,14 @@ __device__ __forceinline__ void view_visibility(const uint32_t (&clo)[7], const 
   visibility_closure(op_lo, op_hi, vis_lo, vis_hi);
 }
 
-// Everything after the view columns: opacity, process_vis, encode, emission.
+// Everything after the view columns and the visibility (view_visibility):
+// encode, emission.
 // out: word-aligned SMEM address at or before this env's record, whose first
 // byte is at misalignment M (warp-uniform, 0..3).  All 7 columns are encoded
 // first; only the emission is specialised on M (one warp-uniform switch), so
 // the four variants share the rest of the code.
 __device__ __forceinline__ void observe_cols(uint32_t (&clo)[7], uint32_t (&chi)[7], uint32_t carry, uint32_t* out,
-                                             int M) {
-  uint32_t vis_lo, vis_hi;
-  view_visibility(clo, chi, vis_lo, vis_hi);
+                                             int M, uint32_t vis_lo, uint32_t vis_hi) {
   // the agent sees what it carries (R#13): view cell (3, 6), always visible
   chi[3] = prmt(chi[3], carry, 0x3410u);
   uint32_t r[7][7];
@@ -473,9 +472,7 @@ __device__ __forceinline__ uint32_t encode4_type(uint32_t w, uint32_t m) {
   return (E & ~D) | (D & 0x04040404u);
 }
 __device__ __forceinline__ void observe_cols_cat(uint32_t (&clo)[7], uint32_t (&chi)[7], uint32_t carry,
-                                                 uint32_t* out, int M) {
-  uint32_t vis_lo, vis_hi;
-  view_visibility(clo, chi, vis_lo, vis_hi);
+                                                 uint32_t* out, int M, uint32_t vis_lo, uint32_t vis_hi) {
   chi[3] = prmt(chi[3], carry, 0x3410u);  // the agent sees what it carries (R#13)
   uint32_t t[14];
 #pragma unroll

@@ -219,6 +219,49 @@ __device__ __forceinline__ void init_reset_queue_counter() {
     if (threadIdx.x == 0) reset_queue_counter() = 0;
 }
 
+// ------------------------------------------------------------------ visibility table
+// Static-layout families (STATIC_LAYOUT: Dynamic-Obstacles, Empty,
+// Empty-Random, DistShift): the layout is the family's template and balls are
+// see-through, so MiniGrid's process_vis mask is a function of the agent pose
+// alone.  Per pose ((ay-1)(W-2) + ax-1) * 4 + dir: (vis_lo, vis_hi) as
+// view_visibility returns them, built by obs_table_kernel with that very
+// function on the template grid.  One table per device (a __device__
+// variable), built at handle creation (navix_create_shard).
+template <int FAM, int H, int W>
+__device__ uint2 g_vis_table[(W - 2) * (H - 2) * 4];
+
+template <int FAM, int H, int W>
+__device__ __forceinline__ const uint2* obs_table_entry(int ax, int ay, int dir) {
+  return g_vis_table<FAM, H, W> + ((ay - 1) * (W - 2) + (ax - 1)) * 4 + dir;
+}
+
+template <int FAM, int H, int W>
+__global__ void __launch_bounds__(TILE) obs_table_kernel() {
+  using C = Cfg<FAM, H, W>;
+  // + 2 zero planes: view_columns_big may read up to two planes past the last
+  // row (the step kernels have other SMEM there; never visible, R#12)
+  __shared__ uint64_t rows_s[C::NPL + 2][TILE];
+  const int tid = threadIdx.x;
+  const int pose = blockIdx.x * TILE + tid;
+  constexpr int NPOSE = (W - 2) * (H - 2) * 4;
+  if (pose >= NPOSE) return;
+  const int dir = pose & 3, cell = pose >> 2;
+  const int ax = 1 + cell % (W - 2), ay = 1 + cell / (W - 2);
+  uint64_t* rows = &rows_s[0][tid];
+#pragma unroll
+  for (int p = 0; p < C::NPL + 2; ++p) rows[p * TILE] = p < H * C::RW ? template_plane<FAM, H, W>(p) : 0ull;
+  uint32_t clo[7], chi[7];
+  if constexpr (C::RW == 1) {
+    if (dir & 1) transpose_lines(rows, rows);
+    view_columns_narrow(rows, ax, ay, dir, clo, chi);
+  } else {
+    view_columns_big<C::RW, H>(rows, ax, ay, dir, clo, chi);
+  }
+  uint32_t vis_lo, vis_hi;
+  view_visibility(clo, chi, vis_lo, vis_hi);
+  g_vis_table<FAM, H, W>[pose] = make_uint2(vis_lo, vis_hi);
+}
+
 // a1-a6 for this thread's env: compute, then write its obs record into s_obs
 // (after before_emit() has made sure s_obs is free).  rows: this env's 8 SMEM
 // row lines (stride TILE); scratch: 8 more lines for the column view of odd
@@ -261,7 +304,13 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // Dynamic-Obstacles: agent-record flag bit 1 = "this env's HBM grid already
   // holds the static template" (balls live outside it), so a reset need not
   // write the template back again
-  bool grid_tmpl = FAM == FAM_DYNOBS && ((rec >> 49) & 1);
+  // Static-layout families (STATIC_LAYOUT, levelgen.cuh: Dynamic-Obstacles,
+  // Empty, Empty-Random, DistShift): agent-record flag bit 1 = "this env's
+  // HBM grid holds the family's template", set by every generated level and
+  // by imports of that layout, cleared by any change of a cell (pickup /
+  // drop / toggle of imported objects); a reset need not write the template
+  // back, and the visibility comes from the per-pose table
+  bool grid_tmpl = STATIC_LAYOUT<FAM> && ((rec >> 49) & 1);
   uint32_t target = FAM == FAM_GOTODOOR ? (uint32_t)(rec >> 56) : 0u;  // GoToDoor target door
 
   float reward = 0.f;
@@ -338,7 +387,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       sc = 0;
       prev_done = false;
       grid_dirty = !grid_tmpl;
-      grid_tmpl = FAM == FAM_DYNOBS;
+      grid_tmpl = STATIC_LAYOUT<FAM>;
     }
   } else if (KC_WARP || (regen && !unified)) {
     // ---- a2: next-step auto-reset (R#18) / reset(key)
@@ -379,7 +428,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       sc = 0;
       prev_done = false;
       grid_dirty = !grid_tmpl;
-      grid_tmpl = FAM == FAM_DYNOBS;
+      grid_tmpl = STATIC_LAYOUT<FAM>;
     }
   }
   // Dynamic-Obstacles on grids up to 8 wide: the transition runs on 64-bit
@@ -592,6 +641,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         *fp = (uint8_t)newf;
         dirty_plane = fy * RW + (fx >> 3);
         grid_dirty = true;
+        grid_tmpl = false;  // no longer the template layout
       }
       if (FAM == FAM_KEYCORRIDOR && is_pick && (carry & 15) == K_BALL) success = true;  // R#8
       if (FAM == FAM_DYNOBS && is_fwd && not_clear) { coll = true; success = false; }  // R#4
@@ -688,6 +738,21 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       transpose_lines(rows, rows);
     }
   }
+  // Dynamic-Obstacles on its static layout (the whole warp): balls are
+  // see-through ([MG] Ball), so the visibility mask depends on the agent pose
+  // alone and comes from a per-pose table (obs_table_kernel) instead of the
+  // opacity gather and the row closures
+  constexpr bool VIS_TABLE = STATIC_LAYOUT<FAM> && !WIDE;
+  bool table_vis = false;
+  uint32_t tvis_lo = 0, tvis_hi = 0;
+  if constexpr (VIS_TABLE) {
+    table_vis = __all_sync(0xffffffffu, !valid || grid_tmpl);
+    if (table_vis && valid) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(obs_table_entry<FAM, H, W>(ax, ay, dir)));
+      tvis_lo = v.x;
+      tvis_hi = v.y;
+    }
+  }
   before_emit();
   {
     uint32_t* const s32 = reinterpret_cast<uint32_t*>(s_obs);
@@ -698,8 +763,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
     else view_columns_big<RW, H>(rows, ax, ay, dir, clo, chi);
     if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
-    if constexpr (OBSK == OBS_CATEGORICAL) observe_cols_cat(clo, chi, carry, s32 + ((le * OB - M) >> 2), M);
-    else observe_cols(clo, chi, carry, s32 + ((le * OB - M) >> 2), M);
+    uint32_t vis_lo, vis_hi;
+    if (table_vis) {
+      vis_lo = tvis_lo;
+      vis_hi = tvis_hi;
+    } else {
+      view_visibility(clo, chi, vis_lo, vis_hi);
+    }
+    if constexpr (OBSK == OBS_CATEGORICAL) observe_cols_cat(clo, chi, carry, s32 + ((le * OB - M) >> 2), M, vis_lo, vis_hi);
+    else observe_cols(clo, chi, carry, s32 + ((le * OB - M) >> 2), M, vis_lo, vis_hi);
   }
 
   EnvResult r;
@@ -1436,6 +1508,11 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       cfg.attrs = attr;
       cfg.numAttrs = env_switch_pdl() ? 1 : 0;
       return cudaLaunchKernelEx(&cfg, navix_step_persistent<FAM, H, W, OBSK>, a);
+    }
+  } else if (mode == MODE_OBS_TABLE) {
+    if constexpr (STATIC_LAYOUT<FAM> && OBSK == OBS_SYMBOLIC) {  // one table for both kinds
+      constexpr int NPOSE = (W - 2) * (H - 2) * 4;
+      obs_table_kernel<FAM, H, W><<<(NPOSE + TILE - 1) / TILE, block, 0, s>>>();
     }
   } else if (mode == MODE_FULL_OBS) {
     full_obs_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);
