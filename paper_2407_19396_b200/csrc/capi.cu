@@ -324,7 +324,8 @@ navix_status navix_create_shard(const char* env_id, int64_t num_envs_total, int6
   {  // scheduler and statistics start at zero even before the first reset
     DeviceGuard dg(device);
     e = cudaMemset(h->state + h->layout.stats_off, 0, h->layout.total - h->layout.stats_off);
-    if (e == cudaSuccess && static_layout_family(h->cfg.family)) {
+    if (e == cudaSuccess && (static_layout_family(h->cfg.family) || h->cfg.family == FAM_LAVAGAP ||
+                             h->cfg.family == FAM_CROSSING || (h->cfg.family == FAM_DOORKEY && h->cfg.width <= 8))) {
       // the per-device visibility table of the static-layout families
       // (step_kernel.cuh obs_table_kernel); idempotent, outside any capture
       KernelArgs a{};
@@ -673,12 +674,46 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
         for (int x = 0; x < W && same; ++x) same = cells[y][x] == template_cell(c, x, y);
       tmpl_flag = same ? 2 : 0;
     }
+    // DoorKey: a generated layout's opaque cells (levelgen.cuh
+    // LAYOUT_KEYED_VIS) — flag bit 2 and byte 7 = (split << 4) | door_y
+    uint64_t layout_key = 0;
+    if (c.family == FAM_DOORKEY && W <= 8) {
+      int split = -1, door_y = -1, doors = 0;
+      bool ok = true;
+      for (int y = 1; y < H - 1 && ok; ++y)
+        for (int x = 1; x < W - 1 && ok; ++x) {
+          const int k = cells[y][x] & 15;
+          const bool door = k == K_DOOR_OPEN || k == K_DOOR_CLOSED || k == K_DOOR_LOCKED;
+          if (k != K_WALL && !door) continue;
+          if (split < 0) split = x;
+          ok = x == split;
+          if (door) { ++doors; door_y = y; }
+        }
+      if (ok && split >= 2 && split <= W - 3 && doors == 1 && door_y >= 1 && door_y <= W - 3) {
+        for (int y = 1; y < H - 1 && ok; ++y) {
+          const int k = cells[y][split] & 15;
+          ok = y == door_y || k == K_WALL;
+        }
+        if (ok) layout_key = (4ull << 48) | ((uint64_t)((split << 4) | door_y) << 56);
+      }
+    }
+    // LavaGap / Crossings (levelgen.cuh BORDER_OPACITY): no door and no opaque
+    // cell inside the border — flag bit 2, key 0
+    if (c.family == FAM_LAVAGAP || c.family == FAM_CROSSING) {
+      bool ok = true;
+      for (int y = 1; y < H - 1 && ok; ++y)
+        for (int x = 1; x < W - 1 && ok; ++x) {
+          const int k = cells[y][x] & 15;
+          ok = k != K_WALL && k != K_DOOR_OPEN && k != K_DOOR_CLOSED && k != K_DOOR_LOCKED;
+        }
+      if (ok) layout_key = 4ull << 48;
+    }
     const int64_t tile = i / TILE, lane = slot_of_env((int)(i % TILE)), si = tile * TILE + lane;
     for (int y = 0; y < H; ++y)
       for (int x = 0; x < W; ++x)
         grid[(size_t)(tile * H * RW + y * RW + x / 8) * TILE + lane] |= (uint64_t)cells[y][x] << (8 * (x % 8));
     agent[si] = (uint64_t)ax | ((uint64_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-               ((uint64_t)sc << 32) | ((uint64_t)(pd | tmpl_flag) << 48) | target;
+               ((uint64_t)sc << 32) | ((uint64_t)(pd | tmpl_flag) << 48) | target | layout_key;
     episode[si] = ep;
     balls[si] = bl;
   }

@@ -32,6 +32,19 @@ template <int FAM>
 constexpr bool STATIC_LAYOUT = FAM == FAM_DYNOBS || FAM == FAM_EMPTY || FAM == FAM_EMPTY_RANDOM ||
                                FAM == FAM_DISTSHIFT1 || FAM == FAM_DISTSHIFT2;
 
+// DoorKey (grids <= 8 wide): the only opaque cells of a generated level are
+// the border, the wall column at x = split and its door at (split, door_y),
+// whose state the agent can toggle; keys, balls, boxes and the goal are
+// see-through and nothing can create an opaque cell.  So the visibility is a
+// function of (pose, split, door_y, door open) (step_kernel.cuh vis table).
+template <int FAM, int W>
+constexpr bool LAYOUT_KEYED_VIS = FAM == FAM_DOORKEY && W <= 8;
+// LavaGap and the lava Crossings: lava is see-through, so a generated level's
+// only opaque cells are the border; with no door in the grid no action can
+// create one.  Their visibility is a function of the pose alone.
+template <int FAM>
+constexpr bool BORDER_OPACITY = FAM == FAM_LAVAGAP || FAM == FAM_CROSSING;
+
 // Static layout plane p (row y = p / RW, cells x = 8 (p % RW) .. +7) as 8
 // cell bytes (cells x >= W are 0 = outside the grid).
 template <int FAM, int H, int W>
@@ -405,6 +418,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     uint32_t kk = ds.next_bounded(cnt - 1);
     if (kk >= ka) ++kk;                            // skip the agent cell
     g.set(1 + (int)(kk % wid), 1 + (int)(kk / wid), make_cell(K_KEY, COL_YELLOW));
+    o.target = (uint32_t)((split << 4) | door_y);  // the opaque layout, for the visibility table
   } else if constexpr (FAM == FAM_LAVAGAP) {
     // [MG] LavaGapEnv._gen_grid
     const int gx = 2 + (int)ds.next_bounded(W - 4);

@@ -227,12 +227,18 @@ __device__ __forceinline__ void init_reset_queue_counter() {
 // view_visibility returns them, built by obs_table_kernel with that very
 // function on the template grid.  One table per device (a __device__
 // variable), built at handle creation (navix_create_shard).
+// DoorKey (LAYOUT_KEYED_VIS): one such table per layout key (split, door_y,
+// door open), key-major.
 template <int FAM, int H, int W>
-__device__ uint2 g_vis_table[(W - 2) * (H - 2) * 4];
+constexpr int vis_table_layouts() {
+  return LAYOUT_KEYED_VIS<FAM, W> ? (W - 4) * (W - 3) * 2 : 1;
+}
+template <int FAM, int H, int W>
+__device__ uint2 g_vis_table[vis_table_layouts<FAM, H, W>() * (W - 2) * (H - 2) * 4];
 
 template <int FAM, int H, int W>
-__device__ __forceinline__ const uint2* obs_table_entry(int ax, int ay, int dir) {
-  return g_vis_table<FAM, H, W> + ((ay - 1) * (W - 2) + (ax - 1)) * 4 + dir;
+__device__ __forceinline__ const uint2* obs_table_entry(int ax, int ay, int dir, int layout = 0) {
+  return g_vis_table<FAM, H, W> + (layout * (W - 2) * (H - 2) + (ay - 1) * (W - 2) + (ax - 1)) * 4 + dir;
 }
 
 template <int FAM, int H, int W>
@@ -242,14 +248,30 @@ __global__ void __launch_bounds__(TILE) obs_table_kernel() {
   // row (the step kernels have other SMEM there; never visible, R#12)
   __shared__ uint64_t rows_s[C::NPL + 2][TILE];
   const int tid = threadIdx.x;
-  const int pose = blockIdx.x * TILE + tid;
+  const int entry = blockIdx.x * TILE + tid;
   constexpr int NPOSE = (W - 2) * (H - 2) * 4;
-  if (pose >= NPOSE) return;
+  if (entry >= vis_table_layouts<FAM, H, W>() * NPOSE) return;
+  const int pose = entry % NPOSE, layout = entry / NPOSE;
   const int dir = pose & 3, cell = pose >> 2;
   const int ax = 1 + cell % (W - 2), ay = 1 + cell / (W - 2);
   uint64_t* rows = &rows_s[0][tid];
+  if constexpr (LAYOUT_KEYED_VIS<FAM, W>) {
+    // border walls, the wall column, its door (locked or open)
+    const int split = 2 + (layout >> 1) / (W - 3), door_y = 1 + (layout >> 1) % (W - 3);
+    const bool open = layout & 1;
+    RowViewT<1> g{rows};
 #pragma unroll
-  for (int p = 0; p < C::NPL + 2; ++p) rows[p * TILE] = p < H * C::RW ? template_plane<FAM, H, W>(p) : 0ull;
+    for (int y = 0; y < 8; ++y) rows[y * TILE] = 0ull;
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        const bool wall = x == 0 || y == 0 || x == W - 1 || y == H - 1 || x == split;
+        g.set(x, y, wall ? CELL_WALL : CELL_EMPTY);
+      }
+    g.set(split, door_y, open ? make_cell(K_DOOR_OPEN, COL_YELLOW) : make_cell(K_DOOR_LOCKED, COL_YELLOW));
+  } else {
+#pragma unroll
+    for (int p = 0; p < C::NPL + 2; ++p) rows[p * TILE] = p < H * C::RW ? template_plane<FAM, H, W>(p) : 0ull;
+  }
   uint32_t clo[7], chi[7];
   if constexpr (C::RW == 1) {
     if (dir & 1) transpose_lines(rows, rows);
@@ -259,7 +281,7 @@ __global__ void __launch_bounds__(TILE) obs_table_kernel() {
   }
   uint32_t vis_lo, vis_hi;
   view_visibility(clo, chi, vis_lo, vis_hi);
-  g_vis_table<FAM, H, W>[pose] = make_uint2(vis_lo, vis_hi);
+  g_vis_table<FAM, H, W>[entry] = make_uint2(vis_lo, vis_hi);
 }
 
 // a1-a6 for this thread's env: compute, then write its obs record into s_obs
@@ -311,7 +333,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // drop / toggle of imported objects); a reset need not write the template
   // back, and the visibility comes from the per-pose table
   bool grid_tmpl = STATIC_LAYOUT<FAM> && ((rec >> 49) & 1);
-  uint32_t target = FAM == FAM_GOTODOOR ? (uint32_t)(rec >> 56) : 0u;  // GoToDoor target door
+  // GoToDoor target door; DoorKey (split << 4) | door_y of its generated layout
+  uint32_t target = (FAM == FAM_GOTODOOR || FAM == FAM_DOORKEY) ? (uint32_t)(rec >> 56) : 0u;
+  // DoorKey: agent-record flag bit 2 = "the layout is a generated DoorKey
+  // layout described by byte 7" (set by generation and by matching imports;
+  // no action can change its opacity except the door's own toggle)
+  // (LavaGap / lava Crossings, BORDER_OPACITY: the same flag says "the only
+  // opaque cells are the border")
+  constexpr bool KEYED_VIS = LAYOUT_KEYED_VIS<FAM, W> || BORDER_OPACITY<FAM>;
+  bool layout_key = KEYED_VIS && ((rec >> 50) & 1);
 
   float reward = 0.f;
   bool term = false, trunc = false, grid_dirty = false;
@@ -422,6 +452,8 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     if (regen) {
       ax = o.ax; ay = o.ay; dir = o.dir;
       target = o.target;
+      layout_key = LAYOUT_KEYED_VIS<FAM, W> ||
+                   (BORDER_OPACITY<FAM> && (FAM != FAM_CROSSING || (a.gen_param & CROSSING_LAVA)));
       balls = o.balls;
       st_fail = o.fail;
       carry = CELL_EMPTY;
@@ -715,7 +747,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     r.tvalid = false;
     r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) |
              ((uint64_t)carry << 24) | ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) |
-             ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)target << 56);
+             ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key ? 1 : 0) << 50) | ((uint64_t)target << 56);
     r.episode = episode;
     r.balls = balls;
     const uint32_t vv = valid && (threadIdx.x % WIDE_LANES) == 0 ? 1u : 0u;  // counted once per env
@@ -725,6 +757,30 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   }
 
   // ---- a6: observation (obs.cuh); odd directions read world columns
+  // Dynamic-Obstacles on its static layout (the whole warp): balls are
+  // see-through ([MG] Ball), so the visibility mask depends on the agent pose
+  // alone and comes from a per-pose table (obs_table_kernel) instead of the
+  // opacity gather and the row closures
+  // (DoorKey: a table per layout key, LAYOUT_KEYED_VIS)
+  constexpr bool VIS_TABLE = (STATIC_LAYOUT<FAM> || KEYED_VIS) && !WIDE;
+  bool table_vis = false;
+  uint32_t tvis_lo = 0, tvis_hi = 0;
+  if constexpr (VIS_TABLE) {
+    table_vis = __all_sync(0xffffffffu, !valid || (KEYED_VIS ? layout_key : grid_tmpl));
+    if (table_vis && valid) {
+      int layout = 0;
+      if constexpr (LAYOUT_KEYED_VIS<FAM, W>) {  // read before odd directions transpose the rows
+        const int split = (int)(target >> 4), door_y = (int)(target & 15);
+        const bool open = (g.get(split, door_y) & 15) == K_DOOR_OPEN;
+        layout = (((split - 2) * (W - 3) + (door_y - 1)) << 1) | (open ? 1 : 0);
+      }
+      // issued early: its latency hides behind the transpose and the view
+      // columns (a load next to its use measured 2 % slower, 42.2 vs 41.3 us)
+      const uint2 v = __ldg(obs_table_entry<FAM, H, W>(ax, ay, dir, layout));
+      tvis_lo = v.x;
+      tvis_hi = v.y;
+    }
+  }
   const uint64_t* lines = rows;
   // rollout: the transposed lines stay valid while the grid does not change
   // (Dynamic-Obstacles moves its balls every step: never cached)
@@ -736,21 +792,6 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       lines = scratch;
     } else {
       transpose_lines(rows, rows);
-    }
-  }
-  // Dynamic-Obstacles on its static layout (the whole warp): balls are
-  // see-through ([MG] Ball), so the visibility mask depends on the agent pose
-  // alone and comes from a per-pose table (obs_table_kernel) instead of the
-  // opacity gather and the row closures
-  constexpr bool VIS_TABLE = STATIC_LAYOUT<FAM> && !WIDE;
-  bool table_vis = false;
-  uint32_t tvis_lo = 0, tvis_hi = 0;
-  if constexpr (VIS_TABLE) {
-    table_vis = __all_sync(0xffffffffu, !valid || grid_tmpl);
-    if (table_vis && valid) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(obs_table_entry<FAM, H, W>(ax, ay, dir)));
-      tvis_lo = v.x;
-      tvis_hi = v.y;
     }
   }
   before_emit();
@@ -783,7 +824,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.dirty = grid_dirty;
   r.tvalid = tvalid;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) |
+           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key ? 1 : 0) << 50) |
            ((uint64_t)target << 56);
   r.episode = episode;
   r.balls = balls;
@@ -1510,9 +1551,10 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       return cudaLaunchKernelEx(&cfg, navix_step_persistent<FAM, H, W, OBSK>, a);
     }
   } else if (mode == MODE_OBS_TABLE) {
-    if constexpr (STATIC_LAYOUT<FAM> && OBSK == OBS_SYMBOLIC) {  // one table for both kinds
-      constexpr int NPOSE = (W - 2) * (H - 2) * 4;
-      obs_table_kernel<FAM, H, W><<<(NPOSE + TILE - 1) / TILE, block, 0, s>>>();
+    if constexpr ((STATIC_LAYOUT<FAM> || LAYOUT_KEYED_VIS<FAM, W> || BORDER_OPACITY<FAM>) &&
+                  OBSK == OBS_SYMBOLIC) {  // both kinds share it
+      constexpr int NENT = vis_table_layouts<FAM, H, W>() * (W - 2) * (H - 2) * 4;
+      obs_table_kernel<FAM, H, W><<<(NENT + TILE - 1) / TILE, block, 0, s>>>();
     }
   } else if (mode == MODE_FULL_OBS) {
     full_obs_kernel<FAM, H, W, OBSK><<<(unsigned)n_tiles, block, 0, s>>>(a, a.obs);

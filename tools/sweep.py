@@ -37,6 +37,8 @@ CONFIGS = [  # (env id, largest N) per BASELINE.json configs
     ("DistShift1-v0", 1 << 20),
     ("SimpleCrossingS9N3-v0", 1 << 20),
     ("SimpleCrossingS11N5-v0", 1 << 20),
+    ("Crossings-S9N3-v0", 1 << 20),
+    ("Crossings-S11N5-v0", 1 << 20),
     ("GoToDoor-8x8-v0", 1 << 20),
     ("FourRooms-v0", 1 << 20),
     ("Dynamic-Obstacles-Random-6x6", 1 << 20),
@@ -49,7 +51,8 @@ CATALOG = ["Empty-5x5-v0", "Empty-6x6-v0", "Empty-8x8-v0", "Empty-16x16-v0", "Em
            "DoorKey-Random-16x16", "FourRooms-v0", "KeyCorridorS3R1-v0", "KeyCorridorS3R2-v0", "KeyCorridorS3R3-v0",
            "KeyCorridorS4R3-v0", "KeyCorridorS5R3-v0", "KeyCorridorS6R3-v0", "LavaGapS5-v0", "LavaGapS6-v0",
            "LavaGapS7-v0", "SimpleCrossingS9N1-v0", "SimpleCrossingS9N2-v0", "SimpleCrossingS9N3-v0",
-           "SimpleCrossingS11N5-v0", "Dynamic-Obstacles-5x5", "Dynamic-Obstacles-6x6", "Dynamic-Obstacles-8x8",
+           "SimpleCrossingS11N5-v0", "Crossings-S9N1-v0", "Crossings-S9N2-v0", "Crossings-S9N3-v0",
+           "Crossings-S11N5-v0", "Dynamic-Obstacles-5x5", "Dynamic-Obstacles-6x6", "Dynamic-Obstacles-8x8",
            "Dynamic-Obstacles-16x16", "DistShift1-v0", "DistShift2-v0", "GoToDoor-5x5-v0", "GoToDoor-6x6-v0",
            "GoToDoor-8x8-v0"]
 CATALOG_SIZES = [1 << 11, 1 << 16, 1 << 20]
