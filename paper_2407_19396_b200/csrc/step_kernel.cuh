@@ -1112,7 +1112,7 @@ constexpr int WIDE_EPC = TILE / WIDE_LANES;  // envs per CTA
 // are OR-reduced over the env's lanes, each lane writes its column's record
 // bytes to SMEM, and each warp copies its 4 envs' records (contiguous,
 // 4-byte aligned) to a.obs.  Called by all lanes of the CTA, converged.
-template <int OBSK>
+template <int FAM, int H, int W, int OBSK>
 __device__ __forceinline__ void wide_observe_and_store(const KernelArgs& a, const EnvResult& r, const uint64_t* rows,
                                                        uint8_t* s_obs) {
   constexpr int OB = obs_record_bytes(OBSK);
@@ -1124,15 +1124,34 @@ __device__ __forceinline__ void wide_observe_and_store(const KernelArgs& a, cons
   uint32_t clo = 0, chi = 0;
   if (j < 7) view_column_narrow(rows, ax, ay, dir, j, clo, chi);
   const int js = j < 7 ? j : 0;
-  uint32_t op_lo = j < 7 ? (clo >> (7 - js)) & (0x01010101u << js) : 0u;  // byte vj, bit vi: opaque
-  uint32_t op_hi = j < 7 ? (chi >> (7 - js)) & (0x01010101u << js) : 0u;
-#pragma unroll
-  for (int k = 1; k < WIDE_LANES; k <<= 1) {  // OR over the env's lanes (aligned groups of 8)
-    op_lo |= __shfl_xor_sync(0xffffffffu, op_lo, k);
-    op_hi |= __shfl_xor_sync(0xffffffffu, op_hi, k);
-  }
   uint32_t vis_lo, vis_hi;
-  visibility_closure(op_lo, op_hi, vis_lo, vis_hi);
+  // the per-pose visibility tables (static layouts, DoorKey, border-only
+  // opacity) when the whole warp qualifies; else the lanes' opacity columns
+  // are OR-reduced and closed
+  constexpr bool KEYED = LAYOUT_KEYED_VIS<FAM, W> || BORDER_OPACITY<FAM>;
+  constexpr bool TABLE = STATIC_LAYOUT<FAM> || KEYED;
+  const bool valid = (int64_t)blockIdx.x * WIDE_EPC + g < a.n;
+  const bool flagged = ((r.nrec >> (KEYED ? 50 : 49)) & 1) != 0;
+  if (TABLE && __all_sync(0xffffffffu, !valid || flagged)) {
+    int layout = 0;
+    if constexpr (LAYOUT_KEYED_VIS<FAM, W>) {
+      const int split = (int)(r.nrec >> 60), door_y = (int)((r.nrec >> 56) & 15);
+      const bool open = (reinterpret_cast<const uint8_t*>(rows)[door_y * TILE * 8 + split] & 15) == K_DOOR_OPEN;
+      layout = valid ? (((split - 2) * (W - 3) + (door_y - 1)) << 1) | (open ? 1 : 0) : 0;
+    }
+    const uint2 v = valid ? __ldg(obs_table_entry<FAM, H, W>(ax, ay, dir, layout)) : make_uint2(0u, 0u);
+    vis_lo = v.x;
+    vis_hi = v.y;
+  } else {
+    uint32_t op_lo = j < 7 ? (clo >> (7 - js)) & (0x01010101u << js) : 0u;  // byte vj, bit vi: opaque
+    uint32_t op_hi = j < 7 ? (chi >> (7 - js)) & (0x01010101u << js) : 0u;
+#pragma unroll
+    for (int k = 1; k < WIDE_LANES; k <<= 1) {  // OR over the env's lanes (aligned groups of 8)
+      op_lo |= __shfl_xor_sync(0xffffffffu, op_lo, k);
+      op_hi |= __shfl_xor_sync(0xffffffffu, op_hi, k);
+    }
+    visibility_closure(op_lo, op_hi, vis_lo, vis_hi);
+  }
   if (j == 3) chi = prmt(chi, carry, 0x3410u);  // the agent sees what it carries (R#13)
   if (j < 7) {
     const uint32_t m_lo = prmt(vis_lo * (1u << (7 - js)), 0u, 0xBA98u);
@@ -1206,7 +1225,7 @@ __global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
   const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(a, tile, rows, nullptr, in, nullptr,
                                                                           NoEmit{}, le);
   __syncwarp();
-  wide_observe_and_store<OBSK>(a, r, rows, s_obs);
+  wide_observe_and_store<FAM, H, W, OBSK>(a, r, rows, s_obs);
   if (valid && j == 0) {
     a.reward[e] = r.reward;
     a.terminated[e] = r.term;
@@ -1267,7 +1286,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_wide(const KernelArgs a, i
     const EnvResult r = tile_compute<FAM, H, W, MODE_STEP, OBSK, NoEmit, true>(
         as, tile, rows, reinterpret_cast<uint64_t*>(s_obs), in, nullptr, NoEmit{}, le);
     __syncwarp();
-    wide_observe_and_store<OBSK>(as, r, rows, s_obs);
+    wide_observe_and_store<FAM, H, W, OBSK>(as, r, rows, s_obs);
     if (valid && j == 0) {
       as.reward[e] = r.reward;
       as.terminated[e] = r.term;
