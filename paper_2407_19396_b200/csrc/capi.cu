@@ -572,7 +572,7 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     if (c.family == FAM_DYNOBS)
       for (int b = 0; b < c.n_obstacles; ++b) {
         const uint32_t p = (uint32_t)(balls[si] >> (8 * b)) & 0xFF;
-        if (p) cells[p & 15][p >> 4] = make_cell(K_BALL, COL_BLUE);
+        if (p) cells[ball_y(c.width, p)][ball_x(c.width, p)] = make_cell(K_BALL, COL_BLUE);
       }
     uint8_t* p = o + (size_t)i * per;
     for (int y = 0; y < c.height; ++y)
@@ -592,8 +592,8 @@ navix_status navix_state_export(navix_env* h, void* host, size_t cap, size_t* wr
     p += 12;
     for (int b = 0; b < c.n_obstacles; ++b, p += 2) {
       const uint32_t q = (uint32_t)(balls[si] >> (8 * b)) & 0xFF;
-      p[0] = (uint8_t)(q >> 4);
-      p[1] = (uint8_t)(q & 15);
+      p[0] = (uint8_t)ball_x(c.width, q);
+      p[1] = (uint8_t)ball_y(c.width, q);
     }
     if (c.family == FAM_GOTODOOR) {  // target door: agent record byte 7 = (x << 4) | y
       p[0] = (uint8_t)(r >> 60);
@@ -650,9 +650,9 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
         return fail(NAVIX_E_INVALID_ARG, "env %lld: obstacle %d at (%d,%d) is not a blue ball", (long long)i, b, bx,
                     by);
       for (int q = 0; q < b; ++q)
-        if (((bl >> (8 * q)) & 0xFF) == (uint64_t)((bx << 4) | by))
+        if (((bl >> (8 * q)) & 0xFF) == (uint64_t)ball_code(W, bx, by))
           return fail(NAVIX_E_INVALID_ARG, "env %lld: duplicate obstacle", (long long)i);
-      bl |= (uint64_t)((bx << 4) | by) << (8 * b);
+      bl |= (uint64_t)ball_code(W, bx, by) << (8 * b);
     }
     uint64_t target = 0;
     if (c.family == FAM_GOTODOOR) {
@@ -662,7 +662,7 @@ navix_status navix_state_import(navix_env* h, const void* host, size_t n_bytes) 
     }
     for (int b = 0; b < c.n_obstacles; ++b) {  // balls live outside the HBM grid
       const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
-      cells[q & 15][q >> 4] = CELL_EMPTY;
+      cells[ball_y(W, q)][ball_x(W, q)] = CELL_EMPTY;
     }
     // static-layout families: agent-record flag bit 1 (layout.h) marks a
     // layout equal to the generator's template (levelgen.cuh template_plane),

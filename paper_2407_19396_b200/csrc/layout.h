@@ -7,7 +7,7 @@
 //                                     cells x >= W are 0
 //   agent   u64 [n_pad]               agent record (below)
 //   episode u32 [n_pad]               episode counter (counter word c1, R#20)
-//   balls   u64 [n_pad]               Dynamic-Obstacles: byte b = (x<<4)|y of ball b (<= 8)
+//   balls   u64 [n_pad]               Dynamic-Obstacles: byte b = ball_code(W, x, y) of ball b (<= 8)
 //   stats   u64 [NSLOT][8]            striped int64 episode statistics
 //   sched   u32 [8 + 4 n_tiles]       persistent step kernel tile scheduler (+ reset-first tile lists)
 // n_pad = num_envs rounded up to TILE.  The struct-of-arrays "row plane"
@@ -24,8 +24,10 @@
 //
 // Agent record (u64, little endian bytes): 0 x, 1 y, 2 dir, 3 carry (cell
 // byte of the carried object, 0x01 = nothing), 4-5 step_count, 6 flags
-// (bit 0 prev_done; bit 1 Dynamic-Obstacles: the HBM grid holds the static
-// template), 7 GoToDoor target door (x << 4) | y (else unused).
+// (bit 0 prev_done; bit 1 static-layout families: the HBM grid holds the
+// family's template; bit 2 DoorKey / LavaGap / Crossings: the visibility
+// table applies, keyed by byte 7 for DoorKey), 7 GoToDoor target door
+// (x << 4) | y, DoorKey (split << 4) | door_y of its generated layout.
 #pragma once
 #include <cstdint>
 
@@ -85,6 +87,15 @@ struct StateLayout {
 };
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Dynamic-Obstacles ball byte (byte b of the balls word = ball b, 0 = none):
+// on grids up to 8 wide the transition's bitboard index 8 y + x, on wider
+// grids (x << 4) | y.  Interior positions never encode to 0.
+__host__ __device__ constexpr uint32_t ball_code(int width, int x, int y) {
+  return width <= 8 ? (uint32_t)(8 * y + x) : (uint32_t)((x << 4) | y);
+}
+__host__ __device__ constexpr int ball_x(int width, uint32_t p) { return width <= 8 ? (int)(p & 7) : (int)(p >> 4); }
+__host__ __device__ constexpr int ball_y(int width, uint32_t p) { return width <= 8 ? (int)(p >> 3) : (int)(p & 15); }
 
 // u64 planes per grid row: 8-byte rows up to width 8, 16-byte rows up to 16 (row f2)
 __host__ __device__ constexpr int row_planes(int width) { return (width + 7) / 8; }

@@ -120,7 +120,7 @@ __device__ __forceinline__ int select64(uint64_t m, uint32_t k) {
 
 struct GenOut {
   int ax, ay, dir;
-  uint64_t balls;  // DynObs: byte b = (x << 4) | y of ball b (up to 8)
+  uint64_t balls;  // DynObs: byte b = ball_code(W, x, y) of ball b (up to 8)
   uint32_t fail;
   uint32_t target;  // GoToDoor: target door (x << 4) | y
 };
@@ -466,7 +466,7 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       }
       const int x = pos % RSB, y = pos / RSB;
       g.set(x, y, make_cell(K_BALL, COL_BLUE));
-      o.balls |= (uint64_t)((x << 4) | y) << (8 * b);
+      o.balls |= (uint64_t)ball_code(W, x, y) << (8 * b);
     }
   } else if constexpr (FAM == FAM_KEYCORRIDOR) {
     // [MG] RoomGrid._gen_grid + KeyCorridorEnv._gen_grid + connect_all

@@ -166,12 +166,18 @@ struct EnvResult {
   uint32_t st[8];
 };
 
+// The state a padding slot (env index >= n in the last tile) is stepped with:
+// its HBM record is never written (caller-owned state buffers hold whatever
+// was there), so it is replaced by a legal pose — (1, 1) east, nothing
+// carried, no flags — and no balls; its results are never stored.
+constexpr uint64_t PADDING_AGENT_RECORD = 0x0000000001000101ull;
+
 // One env's inputs for a step (decoded from the staged tile, or carried in
 // registers across the steps of a rollout).
 struct EnvIn {
   uint64_t rec;      // agent record
   uint32_t act;      // action
-  uint64_t balls;    // DynObs ball positions (byte b = (x << 4) | y)
+  uint64_t balls;    // DynObs ball positions (byte b = ball_code(W, x, y), layout.h)
   uint32_t episode;  // episode counter
   bool episode_known;  // else read from HBM when an auto-reset needs it
   bool tvalid;         // rollout: the scratch lines hold the transpose of these rows
@@ -194,6 +200,10 @@ __device__ __forceinline__ EnvIn decode_staged(const KernelArgs& a, int64_t tile
         in.episode = b.episode[tid];
         in.episode_known = true;
       }
+    }
+    if (e >= a.n) {  // padding slot of the last tile: never written, may hold anything
+      in.rec = PADDING_AGENT_RECORD;
+      in.balls = 0;
     }
   }
   return in;
@@ -478,7 +488,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 #pragma unroll
     for (int bb = 0; bb < C::NOBST; ++bb) {
       const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-      if (p) g.set(p >> 4, p & 15, make_cell(K_BALL, COL_BLUE));
+      if (p) g.set(ball_x(W, p), ball_y(W, p), make_cell(K_BALL, COL_BLUE));
     }
   };
   bool not_clear_pre = false;  // DynObs: the front cell before the motion is not empty / goal
@@ -508,7 +518,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 #pragma unroll
       for (int bb = 0; bb < C::NOBST; ++bb) {
         const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-        bb_balls |= p ? 1ull << (8 * (p & 15) + (p >> 4)) : 0ull;
+        bb_balls |= p ? 1ull << p : 0ull;  // the ball byte is its bit index (ball_code)
       }
       const int fx = ax + (dir == 0 ? 1 : dir == 2 ? -1 : 0), fy = ay + (dir == 1 ? 1 : dir == 3 ? -1 : 0);
       const uint8_t f0 = g.get(fx, fy);
@@ -537,14 +547,14 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
         // transition: the 3x3 box around the ball (interior: starts at bit
         // 8 (by-1) + (bx-1) >= 0); generation: every free cell
-        const int sh = 8 * ((int)(p & 15) - 1) + ((int)(p >> 4) - 1);
+        const int sh = (int)p - 9;  // 8 (by-1) + (bx-1)
         const uint64_t m = gen ? freeb : p ? freeb & (0x070707ull << sh) : 0ull;
         if (m) {
           const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
           const int pos = select64(m, bounded(ub, __popcll(m)));  // k-th admissible cell, row-major
-          const uint64_t old = gen ? 0ull : 1ull << (8 * (p & 15) + (p >> 4));  // empty now
+          const uint64_t old = gen ? 0ull : 1ull << p;  // empty now
           freeb = (freeb | old) & ~(1ull << pos);
-          balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)(((pos & 7) << 4) | (pos >> 3)) << (8 * bb));
+          balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)pos << (8 * bb));  // ball_code = bit index
         } else {
           fails += gen ? 1u : 0u;  // [MG] place_obj would raise; the ball is left out (stats)
         }
@@ -556,7 +566,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
 #pragma unroll
         for (int bb = 0; bb < C::NOBST; ++bb) {
           const uint32_t p = (uint32_t)(balls_before >> (8 * bb)) & 0xFF;
-          if (p) g.set(p >> 4, p & 15, CELL_EMPTY);
+          if (p) g.set(ball_x(W, p), ball_y(W, p), CELL_EMPTY);
         }
       }
     }
@@ -1211,7 +1221,7 @@ __global__ void __launch_bounds__(TILE) navix_step_wide(const KernelArgs a) {
   uint64_t* const rows = &s_rows[0][g];
   // inputs: lane j loads grid row j; every lane the agent record (one
   // broadcast transaction per env); padding envs get a legal dummy state
-  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, FAM == FAM_DYNOBS, false};
+  EnvIn in{PADDING_AGENT_RECORD, 0u, 0ull, 0u, FAM == FAM_DYNOBS, false};
   if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
   if (valid) {
     in.rec = a.agent[slot];
@@ -1256,7 +1266,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_wide(const KernelArgs a, i
   const int le = (int)(e % TILE), st = slot_of_env(le);
   const int64_t slot = tile * TILE + st;
   uint64_t* const rows = &s_rows[0][g];
-  EnvIn in{0x0000000001000101ull /* (1,1) east, nothing carried */, 0u, 0ull, 0u, true, false};
+  EnvIn in{PADDING_AGENT_RECORD, 0u, 0ull, 0u, true, false};
   if (j < H) rows[j * TILE] = valid ? a.grid[(tile * H + j) * TILE + st] : 0ull;
   if (valid) {
     in.rec = a.agent[slot];
@@ -1334,7 +1344,8 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   }
   __syncthreads();
   mbar_wait(mbar, 0);
-  EnvIn in{s_buf.agent[tid], 0u, FAM == FAM_DYNOBS ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
+  EnvIn in{valid ? s_buf.agent[tid] : PADDING_AGENT_RECORD, 0u,
+           FAM == FAM_DYNOBS && valid ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
   bool dirty = false;
   StatsAcc acc;
   // actions from actions[t][n], or drawn in-kernel from the random-policy
@@ -1412,7 +1423,7 @@ __global__ void __launch_bounds__(TILE) full_obs_kernel(const KernelArgs a, uint
 #pragma unroll
     for (int b = 0; b < Cfg<FAM, H, W>::NOBST; ++b) {
       const uint32_t q = (uint32_t)(bl >> (8 * b)) & 0xFF;
-      const int bx = q >> 4, by = q & 15;
+      const int bx = ball_x(W, q), by = ball_y(W, q);
 #pragma unroll
       for (int p = 0; p < H * RW; ++p)
         if (q && p == by * RW + (bx >> 3))

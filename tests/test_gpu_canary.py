@@ -136,3 +136,30 @@ def test_categorical_step_writes_exactly_its_outputs(n, off):
         torch.cuda.synchronize()
         assert all(b.guards_intact() for b in bufs)
         np.testing.assert_array_equal(obs.cpu().numpy(), oo[:, :, :, 0])
+
+
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "Dynamic-Obstacles-8x8-v0", "KeyCorridorS3R3-v0",
+                                    "LavaGapS7-v0", "GoToDoor-8x8-v0", "DoorKey-16x16-v0", "FourRooms-v0"])
+@pytest.mark.parametrize("n", [200, 3000])
+def test_garbage_in_padding_slots(env_id, n):
+    # a caller-owned state buffer starts as random bytes: the padding slots of
+    # the last tile (never written) must not steer any kernel out of bounds
+    from paper_2407_19396_b200 import NavixEnv, state_bytes
+    sb = state_bytes(env_id, n)
+    state = Guarded(sb, 0, 256)
+    state.region().copy_(torch.randint(0, 256, (sb,), dtype=torch.uint8, device="cuda"))
+    g = NavixEnv(env_id, n, seed=9, state=state.region())
+    o = OracleEnv(env_id, n, seed=9)
+    np.testing.assert_array_equal(g.reset().cpu().numpy(), o.reset())
+    acts = random_actions(3, 30, n, o.spec.n_actions)
+    for t in range(20):
+        go, *_ = g.step(torch.from_numpy(acts[t]).cuda())
+        oo, *_ = o.step(acts[t])
+        np.testing.assert_array_equal(go.cpu().numpy(), oo, err_msg=f"step {t}")
+    np.testing.assert_array_equal(g.observe().cpu().numpy(), o.observe())
+    np.testing.assert_array_equal(g.observe_full().cpu().numpy(), o.observe_full())
+    ro = g.rollout(torch.from_numpy(acts[20:30]).cuda())[0]
+    for t in range(10):
+        np.testing.assert_array_equal(ro[t].cpu().numpy(), o.step(acts[20 + t])[0])
+    torch.cuda.synchronize()
+    assert state.guards_intact()
