@@ -2,7 +2,7 @@
 # Round-2 evidence run on the GPU box (one GPU): the GPU suite, the bench line
 # (both arms), sweeps (synchronised and steady state), the ncu launch list and
 # one ncu --set full capture of the headline step kernel.
-OUT=gpurun_out/final
+OUT=${1:-gpurun_out/final}
 mkdir -p $OUT
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/gputests.log 2>&1; echo gputests_rc=$?
 timeout 600 python bench.py > $OUT/bench_line.json 2> $OUT/bench.err; echo bench_rc=$?
