@@ -85,6 +85,15 @@ __host__ __device__ constexpr uint64_t template_free_cells() {
   return m;
 }
 
+// Bitboard of the interior cells (not the border), grids up to 8 wide.
+template <int H, int W>
+__host__ __device__ constexpr uint64_t interior_cells() {
+  uint64_t m = 0;
+  for (int y = 1; y < H - 1 && y < 8; ++y)
+    for (int x = 1; x < W - 1 && x < 8; ++x) m |= 1ull << (8 * y + x);
+  return m;
+}
+
 // Per-thread view of its env's SMEM rows: plane y * RW + x / 8 holds cells
 // x..x+7 of row y (stride TILE between planes).
 template <int RW>

@@ -517,8 +517,9 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       if (act >= 3) act = 0;  // R#7
 #pragma unroll
       for (int bb = 0; bb < C::NOBST; ++bb) {
-        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-        bb_balls |= p ? 1ull << p : 0ull;  // the ball byte is its bit index (ball_code)
+        // the ball byte is its bit index (ball_code); 0 = no ball sets bit 0,
+        // the corner (0, 0), which is neither free nor ever the front cell
+        bb_balls |= 1ull << ((uint32_t)(balls >> (8 * bb)) & 0xFF);
       }
       const int fx = ax + (dir == 0 ? 1 : dir == 2 ? -1 : 0), fy = ay + (dir == 1 ? 1 : dir == 3 ? -1 : 0);
       const uint8_t f0 = g.get(fx, fy);
@@ -541,24 +542,62 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       freeb &= ~bb_balls & ~(1ull << (8 * ay + ax));
       // generation: (env, episode, 0, block 0); transition: (env, episode, 1 << 16 | step, 0)
       const uint4 u = philox4x32_10(make_uint4(genv, episode, gen ? 0u : (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
-      uint32_t fails = 0;
+      // Generation needs no mask: the fixed start's free cells are the
+      // interior minus the agent (1, 1) — the first interior cell — and the
+      // goal (W-2, H-2) — the last —, i.e. interior cells 1 .. NFREE0 in
+      // row-major order, and ball b is cell k_b of that list minus the cells
+      // of the balls before it: one pass over their list indices in ascending
+      // order (gs, kept sorted) steps k_b over each one at or below it.
+      constexpr int IW = W - 2, NFREE0 = (W - 2) * (H - 2) - 2;
+      static_assert(NFREE0 >= C::NOBST && C::NOBST <= 4, "never out of cells; the balls fit the low word");
+      static_assert(template_free_cells<FAM, H, W>() == interior_cells<H, W>() - (1ull << (8 * (H - 2) + W - 2)),
+                    "the template's free cells are the interior minus the goal");
+      uint32_t gs[C::NOBST > 0 ? C::NOBST : 1];
+      uint32_t b32 = (uint32_t)balls;  // byte b = ball b's bit index (0: none)
 #pragma unroll
       for (int bb = 0; bb < C::NOBST; ++bb) {
-        const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
-        // transition: the 3x3 box around the ball (interior: starts at bit
-        // 8 (by-1) + (bx-1) >= 0); generation: every free cell
-        const int sh = (int)p - 9;  // 8 (by-1) + (bx-1)
-        const uint64_t m = gen ? freeb : p ? freeb & (0x070707ull << sh) : 0ull;
-        if (m) {
-          const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
-          const int pos = select64(m, bounded(ub, __popcll(m)));  // k-th admissible cell, row-major
-          const uint64_t old = gen ? 0ull : 1ull << p;  // empty now
-          freeb = (freeb | old) & ~(1ull << pos);
-          balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)pos << (8 * bb));  // ball_code = bit index
+        const uint32_t p = (b32 >> (8 * bb)) & 0xFF;
+        const uint32_t ub = bb == 0 ? u.x : bb == 1 ? u.y : bb == 2 ? u.z : u.w;
+        // transition: the 3x3 box around the ball, from bit 8 (by-1) + (bx-1)
+        // = p - 9 (interior ball: p >= 9), as three 3-bit rows of a word
+        const int sh = (int)p - 9;
+        const uint32_t box = p ? (uint32_t)(freeb >> (sh & 63)) & 0x070707u : 0u;
+        const uint32_t n = gen ? (uint32_t)(NFREE0 - bb) : (uint32_t)__popc(box);
+        const uint32_t k = bounded(ub, n);  // k-th admissible cell, row-major
+        int pos;
+        if (gen) {
+          uint32_t i = k;
+#pragma unroll
+          for (int j = 0; j < bb; ++j) i += gs[j] <= i ? 1u : 0u;
+          if (bb + 1 < C::NOBST) {  // insert i into the sorted list
+            uint32_t x = i;
+#pragma unroll
+            for (int j = 0; j < bb; ++j) {
+              const uint32_t lo = min(gs[j], x);
+              x = max(gs[j], x);
+              gs[j] = lo;
+            }
+            gs[bb] = x;
+          }
+          const uint32_t q = i + 1u;  // interior cell q (0 = the agent's) = bit 9 + q + (8 - IW) (q / IW)
+          pos = (int)(9u + q + (8u - IW) * (q / IW));
         } else {
-          fails += gen ? 1u : 0u;  // [MG] place_obj would raise; the ball is left out (stats)
+          // the k-th set bit of the box: its row, then its column
+          const uint32_t c0 = __popc(box & 0x7u), c1 = __popc(box & 0x707u);
+          const bool ge0 = k >= c0, ge1 = k >= c1;
+          const uint32_t r8 = (ge0 ? 8u : 0u) + (ge1 ? 8u : 0u);
+          const uint32_t kr = k - (ge1 ? c1 : ge0 ? c0 : 0u);
+          const uint32_t row = (box >> r8) & 0x7u;
+          const uint32_t col = (kr >= (row & 1u) ? 1u : 0u) + (kr >= (uint32_t)__popc(row & 3u) ? 1u : 0u);
+          pos = sh + (int)(r8 + col);
+        }
+        if (n) {  // (always for generation: NFREE0 >= NOBST)
+          if (!gen) freeb = (freeb | (1ull << p)) & ~(1ull << pos);  // the old cell is empty now
+          b32 = __byte_perm(b32, (uint32_t)pos, (0x3210u & ~(0xFu << (4 * bb))) | (4u << (4 * bb)));
         }
       }
+      balls = b32;
+      const uint32_t fails = 0;
       if (gen) st_fail = fails;
       if (scratch != nullptr && balls != balls_before) {
         // rollout: the SMEM rows persist across steps and hold last step's
