@@ -181,6 +181,7 @@ struct EnvIn {
   uint32_t episode;  // episode counter
   bool episode_known;  // else read from HBM when an auto-reset needs it
   bool tvalid;         // rollout: the scratch lines hold the transpose of these rows
+  bool rows_persist;   // rollout: the SMEM rows are last step's (not reloaded from HBM)
 };
 
 template <int FAM, int MODE, int NPL>
@@ -377,7 +378,11 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // resetting lanes place their balls in the same bitboard loop that moves
   // the other lanes' balls, so they need neither the queue nor the generator
   constexpr bool BITBOARD = FAM == FAM_DYNOBS && RW == 1 && MODE == MODE_STEP;
-  const bool unified = BITBOARD && a.gen_param == 0;  // grid-uniform
+  // Wider fixed-start Dynamic-Obstacles grids (16x16) generate in place too:
+  // the resetting lanes place their balls by list index (below, no mask, no
+  // queue), the other lanes move theirs on the SMEM rows (a3)
+  constexpr bool UNIFIED_ROWS = FAM == FAM_DYNOBS && RW > 1 && MODE == MODE_STEP && !WIDE;
+  const bool unified = (BITBOARD || UNIFIED_ROWS) && a.gen_param == 0;  // grid-uniform
   if (COMPACT && !unified) {
     // Agent record st of the staging this tile has consumed holds (episode |
     // generator output << 32) (each thread overwrites only the record it
@@ -611,6 +616,74 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     }
     if (!regen || gen) overlay_balls();  // (queue-generated levels already hold theirs)
   }
+  // Dynamic-Obstacles draws of this step, one Philox block per 4 balls:
+  // generation (env, episode, 0, block) — the level generator's stream —,
+  // transition (env, episode, 1 << 16 | step, block)
+  constexpr int DYN_NB = UNIFIED_ROWS ? (C::NOBST + 3) / 4 : 1;
+  uint4 dyn_u[DYN_NB];
+  if constexpr (UNIFIED_ROWS) {
+    const bool gen = unified && regen;
+    if (gen) {
+      // a2 (R#18): episode e+1 of [MG] DynamicObstaclesEnv, agent (1,1) east
+      episode = (in.episode_known ? episode : a.episode[slot]) + 1u;
+      ax = 1; ay = 1; dir = 0;
+      carry = CELL_EMPTY;
+      sc = 0;
+      prev_done = false;
+      if (!grid_tmpl) {  // an imported layout: back to the template (SMEM now, HBM at write-back)
+#pragma unroll
+        for (int q = 0; q < H * RW; ++q) rows[q * TILE] = template_plane<FAM, H, W>(q);
+      } else if (in.rows_persist) {
+        // rollout: the SMEM rows persist across steps and hold the last
+        // episode's balls; their cells are empty in the static layout
+#pragma unroll
+        for (int bb = 0; bb < C::NOBST; ++bb) {
+          const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
+          if (p) g.set(ball_x(W, p), ball_y(W, p), CELL_EMPTY);
+        }
+      }
+      grid_dirty = !grid_tmpl;
+      grid_tmpl = true;
+      st_fail = 0;
+    }
+    if (gen || !regen) {
+#pragma unroll
+      for (int k = 0; k < DYN_NB; ++k)
+        dyn_u[k] = philox4x32_10(make_uint4(genv, episode, gen ? 0u : (1u << 16) | sc, (uint32_t)k), a.key_lo, a.key_hi);
+    }
+    if (gen) {
+      // the fixed start's free cells are interior cells 1 .. NFREE0 in
+      // row-major order (0 is the agent's, the last the goal's); ball b is
+      // cell k_b of that list minus those of the balls before it (one pass
+      // over their list indices gs, kept sorted, as the BITBOARD loop)
+      constexpr int IW = W - 2, NFREE0 = (W - 2) * (H - 2) - 2;
+      static_assert(NFREE0 >= C::NOBST, "the generator never runs out of cells here");
+      uint32_t gs[C::NOBST > 0 ? C::NOBST : 1];
+      balls = 0;
+#pragma unroll
+      for (int bb = 0; bb < C::NOBST; ++bb) {
+        const uint4& x = dyn_u[bb >> 2];
+        const uint32_t ub = (bb & 3) == 0 ? x.x : (bb & 3) == 1 ? x.y : (bb & 3) == 2 ? x.z : x.w;
+        uint32_t i = bounded(ub, (uint32_t)(NFREE0 - bb));
+#pragma unroll
+        for (int j = 0; j < bb; ++j) i += gs[j] <= i ? 1u : 0u;
+        if (bb + 1 < C::NOBST) {
+          uint32_t v = i;
+#pragma unroll
+          for (int j = 0; j < bb; ++j) {
+            const uint32_t lo = min(gs[j], v);
+            v = max(gs[j], v);
+            gs[j] = lo;
+          }
+          gs[bb] = v;
+        }
+        const uint32_t q = i + 1u;  // interior cell q
+        const int bx = 1 + (int)(q % IW), by = 1 + (int)(q / IW);
+        balls |= (uint64_t)ball_code(W, bx, by) << (8 * bb);
+      }
+      overlay_balls();
+    }
+  }
   if (!regen) {
     if (FAM == FAM_DYNOBS && !BITBOARD) overlay_balls();
     if (MODE == MODE_STEP) {
@@ -629,8 +702,10 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         uint4 u = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int bb = 0; bb < C::NOBST; ++bb) {
-          if ((bb & 3) == 0)
-            u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, (uint32_t)(bb >> 2)), a.key_lo, a.key_hi);
+          if ((bb & 3) == 0) {
+            if constexpr (UNIFIED_ROWS) u = dyn_u[bb >> 2];  // drawn above
+            else u = philox4x32_10(make_uint4(genv, episode, (1u << 16) | sc, (uint32_t)(bb >> 2)), a.key_lo, a.key_hi);
+          }
           const uint32_t p = (uint32_t)(balls >> (8 * bb)) & 0xFF;
           if (!p) continue;
           const int bx = p >> 4, by = p & 15;
@@ -1384,7 +1459,7 @@ __global__ void __launch_bounds__(TILE) navix_rollout_kernel(const KernelArgs a,
   __syncthreads();
   mbar_wait(mbar, 0);
   EnvIn in{valid ? s_buf.agent[tid] : PADDING_AGENT_RECORD, 0u,
-           FAM == FAM_DYNOBS && valid ? s_buf.balls[tid] : 0ull, a.episode[slot], true};
+           FAM == FAM_DYNOBS && valid ? s_buf.balls[tid] : 0ull, a.episode[slot], true, false, true};
   bool dirty = false;
   StatsAcc acc;
   // actions from actions[t][n], or drawn in-kernel from the random-policy
