@@ -94,6 +94,26 @@ __host__ __device__ constexpr uint64_t interior_cells() {
   return m;
 }
 
+// 0xFF in byte i of the result iff bit i of b (b < 256): each half
+// replicates its 4 bits to 4 bytes, keeps bit i in byte i, and the byte's
+// sign after + 0x7F (no carry out: bytes <= 8) is replicated by a byte permute.
+__device__ __forceinline__ uint64_t bits_to_bytes(uint32_t b) {
+  uint32_t lo = ((b & 0xFu) * 0x01010101u & 0x08040201u) + 0x7F7F7F7Fu;
+  uint32_t hi = ((b >> 4) * 0x01010101u & 0x08040201u) + 0x7F7F7F7Fu;
+  asm("prmt.b32 %0, %0, 0, 0xBA98;" : "+r"(lo));
+  asm("prmt.b32 %0, %0, 0, 0xBA98;" : "+r"(hi));
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// Byte mask of the interior cells (1 <= x <= W-2) of row plane q (cells 8q .. 8q+7).
+template <int W>
+__host__ __device__ constexpr uint64_t interior_bytes(int q) {
+  uint64_t m = 0;
+  for (int i = 0; i < 8; ++i)
+    if (8 * q + i >= 1 && 8 * q + i <= W - 2) m |= 0xFFull << (8 * i);
+  return m;
+}
+
 // Per-thread view of its env's SMEM rows: plane y * RW + x / 8 holds cells
 // x..x+7 of row y (stride TILE between planes).
 template <int RW>
@@ -379,11 +399,24 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
       const uint32_t bit = 1u << (2 * ((b & 7) + 1));
       if (b & 8) hmask |= bit; else vmask |= bit;
     }
+    // the rivers, a whole row plane at a time: plane q of an interior row is
+    // obstacle at the interior bytes if the row is a horizontal river, else at
+    // the vertical rivers' bytes (a byte mask spread from vmask's bits)
+    {
+      const uint64_t obst8 = 0x0101010101010101ull * obstacle;
+      uint64_t vm[C::RW];
 #pragma unroll
-    for (int y = 1; y < H - 1; ++y)
+      for (int q = 0; q < C::RW; ++q) vm[q] = bits_to_bytes((vmask >> (8 * q)) & 0xFFu);
 #pragma unroll
-      for (int x = 1; x < W - 1; ++x)
-        if (((hmask >> y) & 1u) | ((vmask >> x) & 1u)) g.set(x, y, obstacle);
+      for (int y = 1; y < H - 1; ++y) {
+        const bool hr = (hmask >> y) & 1u;
+#pragma unroll
+        for (int q = 0; q < C::RW; ++q) {
+          const uint64_t m = hr ? interior_bytes<W>(q) : vm[q];
+          g.rows[(y * C::RW + q) * TILE] = (template_plane<FAM, H, W>(y * C::RW + q) & ~m) | (obst8 & m);
+        }
+      }
+    }
     // path: popc(vmask) 'h' moves then popc(hmask) 'v' moves (bit k = 1: 'v'), Fisher-Yates
     const int nv = __popc(vmask);
     uint32_t path = ((1u << N) - 1) & ~((1u << nv) - 1);
