@@ -517,19 +517,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     }
     const bool warp_tmpl = __all_sync(0xffffffffu, grid_tmpl);
     const bool move = !regen;
-    uint64_t bb_balls = 0;
-    if (move) {
-      if (act >= 3) act = 0;  // R#7
-#pragma unroll
-      for (int bb = 0; bb < C::NOBST; ++bb) {
-        // the ball byte is its bit index (ball_code); 0 = no ball sets bit 0,
-        // the corner (0, 0), which is neither free nor ever the front cell
-        bb_balls |= 1ull << ((uint32_t)(balls >> (8 * bb)) & 0xFF);
-      }
-      const int fx = ax + (dir == 0 ? 1 : dir == 2 ? -1 : 0), fy = ay + (dir == 1 ? 1 : dir == 3 ? -1 : 0);
-      const uint8_t f0 = g.get(fx, fy);
-      not_clear_pre = (f0 != CELL_EMPTY && (f0 & 15) != K_GOAL) || ((bb_balls >> (8 * fy + fx)) & 1ull);
-    }
+    if (move && act >= 3) act = 0;  // R#7
     if (move || gen) {
       // admissible cells: empty in the static layout, no ball, not the agent
       uint64_t freeb;
@@ -544,7 +532,19 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
           freeb |= (((z >> 7) * 0x0102040810204080ull) >> 56) << (8 * y);  // bit x: byte x == 0
         }
       }
-      freeb &= ~bb_balls & ~(1ull << (8 * ay + ax));
+      // the ball byte is its bit index (ball_code); 0 = no ball clears bit 0,
+      // the corner (0, 0), which is never free
+#pragma unroll
+      for (int bb = 0; bb < C::NOBST; ++bb) freeb &= ~(1ull << ((uint32_t)(balls >> (8 * bb)) & 0xFF));
+      freeb &= ~(1ull << (8 * ay + ax));
+      if (move) {
+        // a3's front cell before the motion: not clear unless empty and no
+        // ball (a free bit: the agent's own cell is not in front of it) or the
+        // goal (never under a ball)
+        const int fx = ax + (dir == 0 ? 1 : dir == 2 ? -1 : 0), fy = ay + (dir == 1 ? 1 : dir == 3 ? -1 : 0);
+        const uint8_t f0 = g.get(fx, fy);
+        not_clear_pre = (f0 & 15) != K_GOAL && !((freeb >> (8 * fy + fx)) & 1ull);
+      }
       // generation: (env, episode, 0, block 0); transition: (env, episode, 1 << 16 | step, 0)
       const uint4 u = philox4x32_10(make_uint4(genv, episode, gen ? 0u : (1u << 16) | sc, 0u), a.key_lo, a.key_hi);
       // Generation needs no mask: the fixed start's free cells are the
