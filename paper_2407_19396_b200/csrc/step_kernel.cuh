@@ -366,11 +366,15 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // level generator for a few lanes.  Their resetting envs are queued per CTA
   // instead and generated by the first threads (one warp for up to 32 of
   // them), each into its env's SMEM rows.
-  // (measured with the queue on every Dynamic-Obstacles width, round-1 close:
-  // DynObs-16x16 198 -> 174 us per 2^20-env step, 14.6 -> 12.5 us at 2^16.
-  // A warp-local queue — ballot, one generator pass per warp, no CTA barrier —
+  // The queue now serves GoToDoor and the Dynamic-Obstacles-Random ids: the
+  // fixed-start Dynamic-Obstacles ids generate in place without a generator
+  // call (BITBOARD / UNIFIED_ROWS below; DynObs-16x16 174 -> 126.5 us per
+  // 2^20-env step against the queue, which had itself taken it from 198).
+  // (A warp-local queue — ballot, one generator pass per warp, no CTA barrier —
   // measured worse, DynObs-8x8 79 -> 91 us at 2^20: four passes per tile
-  // instead of one, on an ALU-pipe-bound kernel.)
+  // instead of one, on an ALU-pipe-bound kernel.  GoToDoor's 4 Philox blocks
+  // per level computed by the whole CTA ahead of the generator pass, through
+  // s_obs: 67.7 -> 69.3 us at 2^20, an extra barrier for no shorter pass.)
   constexpr bool COMPACT = (FAM == FAM_DYNOBS || FAM == FAM_GOTODOOR) && MODE == MODE_STEP && !WIDE;
   constexpr bool KC_WARP = FAM == FAM_KEYCORRIDOR && MODE == MODE_STEP && !WIDE;
   constexpr int KC_WARP_MAX = NAVIX_KC_WARP_MAX;
