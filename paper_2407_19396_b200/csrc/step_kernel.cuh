@@ -748,20 +748,24 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
           if ((unsigned)adx < 3u && (unsigned)ady < 3u) m &= ~(1u << (4 * ady + adx));
           if (m) {
             const uint32_t ub = (bb & 3) == 0 ? u.x : (bb & 3) == 1 ? u.y : (bb & 3) == 2 ? u.z : u.w;
-            uint32_t kk = bounded(ub, __popc(m)), k = 0;  // kk-th set bit (row-major order)
-            uint32_t c = __popc(m & 0xFFu);
-            if (kk >= c) { kk -= c; k = 8; }
-            const uint32_t mm = m >> k;
-            c = __popc(mm & 0xFu);
-            if (kk >= c) { kk -= c; k += 4; }
-            const uint32_t m4 = m >> k;
-            c = __popc(m4 & 0x3u);
-            if (kk >= c) { kk -= c; k += 2; }
-            k += kk >= ((m >> k) & 1u) ? 1u : 0u;
-            const int nx = bx - 1 + (int)(k & 3), ny = by - 1 + (int)(k >> 2);
+            // the k-th set bit (row-major order): its row (two prefix
+            // popcounts of the 4-bit rows), then its column
+            const uint32_t k = bounded(ub, __popc(m));
+            const uint32_t c0 = __popc(m & 0xFu), c1 = __popc(m & 0xFFu);
+            const bool ge0 = k >= c0, ge1 = k >= c1;
+            const uint32_t r = (ge0 ? 1u : 0u) + (ge1 ? 1u : 0u);
+            const uint32_t kr = k - (ge1 ? c1 : ge0 ? c0 : 0u);
+            const uint32_t row = (m >> (4 * r)) & 0x7u;
+            const uint32_t col = (kr >= (row & 1u) ? 1u : 0u) + (kr >= (uint32_t)__popc(row & 3u) ? 1u : 0u);
+            const int nx = bx - 1 + (int)col, ny = by - 1 + (int)r;
             g.set(nx, ny, make_cell(K_BALL, COL_BLUE));
             g.set(bx, by, CELL_EMPTY);
-            balls = (balls & ~(0xFFull << (8 * bb))) | ((uint64_t)((nx << 4) | ny) << (8 * bb));
+            // ball byte bb = ball_code (x << 4 | y on these grids): one byte
+            // permute on the word holding it
+            const uint32_t code = ((uint32_t)nx << 4) | (uint32_t)ny;
+            const uint32_t SEL = (0x3210u & ~(0xFu << (4 * (bb & 3)))) | (4u << (4 * (bb & 3)));
+            if (bb < 4) balls = (balls & 0xFFFFFFFF00000000ull) | __byte_perm((uint32_t)balls, code, SEL);
+            else balls = (balls & 0xFFFFFFFFull) | ((uint64_t)__byte_perm((uint32_t)(balls >> 32), code, SEL) << 32);
           }
         }
       }
