@@ -353,6 +353,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   // opaque cells are the border")
   constexpr bool KEYED_VIS = LAYOUT_KEYED_VIS<FAM, W> || BORDER_OPACITY<FAM>;
   bool layout_key = KEYED_VIS && ((rec >> 50) & 1);
+  // GoToDoor: the same flag says "a generated room, no door opened since":
+  // the room's walls and closed doors enclose the agent, so no cell outside
+  // the room — and no position outside the grid — can become visible
+  // (process_vis only spreads from visible see-through cells, all inside the
+  // room), and the view needs no out-of-grid walls (R#37)
+  bool room_closed = FAM == FAM_GOTODOOR && ((rec >> 50) & 1);
 
   float reward = 0.f;
   bool term = false, trunc = false, grid_dirty = false;
@@ -428,8 +434,12 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
       const uint64_t qr = q_rec[tid];
       const uint32_t o = (uint32_t)(qr >> 32);
       episode = (uint32_t)qr;
-      if (FAM == FAM_GOTODOOR) target = o >> 24;
-      else balls = q_balls[tid];
+      if (FAM == FAM_GOTODOOR) {
+        target = o >> 24;
+        room_closed = true;
+      } else {
+        balls = q_balls[tid];
+      }
       ax = (int)(o & 0xFF); ay = (int)((o >> 8) & 0xFF); dir = (int)((o >> 16) & 3);
       st_fail = (o >> 18) & 63u;
       carry = CELL_EMPTY;
@@ -471,6 +481,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     if (regen) {
       ax = o.ax; ay = o.ay; dir = o.dir;
       target = o.target;
+      room_closed = FAM == FAM_GOTODOOR;
       layout_key = LAYOUT_KEYED_VIS<FAM, W> ||
                    (BORDER_OPACITY<FAM> && (FAM != FAM_CROSSING || (a.gen_param & CROSSING_LAVA)));
       balls = o.balls;
@@ -806,6 +817,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
         dirty_plane = fy * RW + (fx >> 3);
         grid_dirty = true;
         grid_tmpl = false;  // no longer the template layout
+        room_closed = false;  // GoToDoor: a door opened
       }
       if (FAM == FAM_KEYCORRIDOR && is_pick && (carry & 15) == K_BALL) success = true;  // R#8
       if (FAM == FAM_DYNOBS && is_fwd && not_clear) { coll = true; success = false; }  // R#4
@@ -879,7 +891,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     r.tvalid = false;
     r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) |
              ((uint64_t)carry << 24) | ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) |
-             ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key ? 1 : 0) << 50) | ((uint64_t)target << 56);
+             ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key || room_closed ? 1 : 0) << 50) | ((uint64_t)target << 56);
     r.episode = episode;
     r.balls = balls;
     const uint32_t vv = valid && (threadIdx.x % WIDE_LANES) == 0 ? 1u : 0u;  // counted once per env
@@ -935,7 +947,9 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
     uint32_t clo[7], chi[7];
     if constexpr (RW == 1) view_columns_narrow(lines, ax, ay, dir, clo, chi);
     else view_columns_big<RW, H>(rows, ax, ay, dir, clo, chi);
-    if constexpr (FAM == FAM_GOTODOOR) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
+    if constexpr (FAM == FAM_GOTODOOR) {
+      if (!room_closed) view_oob_walls<H, W>(ax, ay, dir, clo, chi);  // R#37
+    }
     uint32_t vis_lo, vis_hi;
     if (table_vis) {
       vis_lo = tvis_lo;
@@ -956,7 +970,7 @@ __device__ __forceinline__ EnvResult tile_compute(const KernelArgs& a, int64_t t
   r.dirty = grid_dirty;
   r.tvalid = tvalid;
   r.nrec = (uint64_t)(uint32_t)ax | ((uint64_t)(uint32_t)ay << 8) | ((uint64_t)dir << 16) | ((uint64_t)carry << 24) |
-           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key ? 1 : 0) << 50) |
+           ((uint64_t)sc << 32) | ((uint64_t)(prev_done ? 1 : 0) << 48) | ((uint64_t)(grid_tmpl ? 1 : 0) << 49) | ((uint64_t)(layout_key || room_closed ? 1 : 0) << 50) |
            ((uint64_t)target << 56);
   r.episode = episode;
   r.balls = balls;

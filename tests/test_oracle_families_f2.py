@@ -368,6 +368,34 @@ def test_gotodoor_open_edge_walk_blocked_outside():
     assert (rec[75], rec[76]) == (0, 2) and te[0] == 0
 
 
+@pytest.mark.parametrize("S", [5, 6, 8])
+def test_gotodoor_closed_room_never_sees_outside_the_grid(S):
+    # R#37: a generated room with its doors closed encloses the agent, and
+    # [MG] process_vis only spreads from visible see-through cells, so no view
+    # position outside the grid is ever visible (the kernels skip the
+    # out-of-grid walls for such rooms).  Every action but toggle (which opens
+    # a door and ends the episode); done ends episodes, so new rooms come too.
+    n, T = 300, 40
+    env = OracleEnv(f"GoToDoor-{S}x{S}-v0", n, seed=5)
+    obs = env.reset()
+    rng = np.random.default_rng(0)
+    vi, vj = np.meshgrid(np.arange(7), np.arange(7), indexing="ij")
+    fwd = np.array([(1, 0), (0, 1), (-1, 0), (0, -1)])
+    checked = 0
+    for _ in range(T):
+        rec = env.export().astype(np.int64)
+        ax, ay, d = rec[:, 3 * S * S], rec[:, 3 * S * S + 1], rec[:, 3 * S * S + 2]
+        fx, fy = fwd[d, 0][:, None, None], fwd[d, 1][:, None, None]
+        lx, ly = -fy, fx  # view column vi lies at lateral offset vi - 3, row vj at distance 6 - vj
+        x = ax[:, None, None] + (6 - vj) * fx + (vi - 3) * lx
+        y = ay[:, None, None] + (6 - vj) * fy + (vi - 3) * ly
+        out = (x < 0) | (x >= S) | (y < 0) | (y >= S)
+        assert not obs[out].any()
+        checked += int(out.sum())
+        obs, *_ = env.step(rng.choice([0, 1, 2, 3, 4, 6], size=n).astype(np.uint8))
+    assert checked > 10000
+
+
 # ---------------------------------------------------------------- FourRooms
 def test_fourrooms_structure_and_uniform_placement():
     s = spec_of("Navix-FourRooms-v0")
