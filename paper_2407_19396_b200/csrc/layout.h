@@ -26,7 +26,8 @@
 // byte of the carried object, 0x01 = nothing), 4-5 step_count, 6 flags
 // (bit 0 prev_done; bit 1 static-layout families: the HBM grid holds the
 // family's template; bit 2 DoorKey / LavaGap / Crossings: the visibility
-// table applies, keyed by byte 7 for DoorKey), 7 GoToDoor target door
+// table applies, keyed by byte 7 for DoorKey; GoToDoor: a generated room
+// with its doors still closed, so the view needs no out-of-grid walls), 7 GoToDoor target door
 // (x << 4) | y, DoorKey (split << 4) | door_y of its generated layout.
 #pragma once
 #include <cstdint>
