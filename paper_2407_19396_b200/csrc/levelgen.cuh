@@ -278,6 +278,82 @@ __device__ __forceinline__ D make_draws(D*, uint32_t env, uint32_t ep, uint32_t 
   return D(env, ep, klo, khi);
 }
 
+// [MG] CrossingEnv._gen_grid, obstacle Wall or Lava (gparam & CROSSING_LAVA),
+// N crossings (NC > 0: N == NC, a compile-time constant, loops unrolled); the
+// two shuffles as R#35 reads them.  Rivers are nibbles (bit 3: horizontal,
+// bits 0-2: position / 2 - 1): (S-3)/2 vertical ones, then as many horizontal.
+template <int H, int W, int NC, class Draws>
+__device__ __forceinline__ void crossing_level(RowViewT<Cfg<FAM_CROSSING, H, W>::RW> g, Draws& ds, int N_,
+                                               uint8_t obstacle) {
+  using C = Cfg<FAM_CROSSING, H, W>;
+  constexpr int FAM = FAM_CROSSING;
+  constexpr int NRV = (W - 3) / 2, M = 2 * NRV;
+  const int N = NC > 0 ? NC : N_;
+  constexpr int NU = NC > 0 ? NC : 1;  // unroll factor of the N-long loops
+  using RivT = typename std::conditional<(M <= 8), uint32_t, uint64_t>::type;
+  RivT riv = 0;
+#pragma unroll
+  for (int k = 0; k < M; ++k) riv |= (RivT)((k < NRV ? 0 : 8) | (k % NRV)) << (4 * k);
+  uint32_t vmask = 0, hmask = 0;  // bit p: a vertical river at x = p / a horizontal one at y = p
+#pragma unroll NU
+  for (int k = 0; k < N; ++k) {
+    const int j = k + (int)ds.next_bounded((uint32_t)(M - k));
+    const RivT a = (riv >> (4 * k)) & 15, b = (riv >> (4 * j)) & 15;
+    riv = (riv & ~((RivT)15 << (4 * k)) & ~((RivT)15 << (4 * j))) | (b << (4 * k)) | (a << (4 * j));
+    const uint32_t bit = 1u << (2 * (((uint32_t)b & 7) + 1));
+    if (b & 8) hmask |= bit; else vmask |= bit;
+  }
+  // the rivers, a whole row plane at a time: plane q of an interior row is
+  // obstacle at the interior bytes if the row is a horizontal river, else at
+  // the vertical rivers' bytes (a byte mask spread from vmask's bits)
+  {
+    const uint64_t obst8 = 0x0101010101010101ull * obstacle;
+    uint64_t vm[C::RW];
+#pragma unroll
+    for (int q = 0; q < C::RW; ++q) vm[q] = bits_to_bytes((vmask >> (8 * q)) & 0xFFu);
+#pragma unroll
+    for (int y = 1; y < H - 1; ++y) {
+      const bool hr = (hmask >> y) & 1u;
+#pragma unroll
+      for (int q = 0; q < C::RW; ++q) {
+        const uint64_t m = hr ? interior_bytes<W>(q) : vm[q];
+        g.rows[(y * C::RW + q) * TILE] = (template_plane<FAM, H, W>(y * C::RW + q) & ~m) | (obst8 & m);
+      }
+    }
+  }
+  // path: popc(vmask) 'h' moves then popc(hmask) 'v' moves (bit k = 1: 'v'), Fisher-Yates
+  const int nv = __popc(vmask);
+  uint32_t path = ((1u << N) - 1) & ~((1u << nv) - 1);
+#pragma unroll NU
+  for (int t = 0; t < N - 1; ++t) {
+    const int i = N - 1 - t;
+    const int j = (int)ds.next_bounded((uint32_t)(i + 1));
+    const uint32_t bi = (path >> i) & 1u, bj = (path >> j) & 1u;
+    path = (path & ~(1u << i) & ~(1u << j)) | (bj << i) | (bi << j);
+  }
+  // openings: the current room spans x in (xlo, xhi), y in (ylo, yhi)
+  auto next_limit = [](uint32_t m, int lo, int end) {
+    const uint32_t above = m & ~((2u << lo) - 1);
+    return above ? __ffs(above) - 1 : end;
+  };
+  int xlo = 0, ylo = 0;
+  int xhi = next_limit(vmask, 0, W - 1), yhi = next_limit(hmask, 0, H - 1);
+#pragma unroll NU
+  for (int k = 0; k < N; ++k) {
+    if (((path >> k) & 1u) == 0) {  // 'h': through the vertical river at x = xhi
+      const int y = ylo + 1 + (int)ds.next_bounded((uint32_t)(yhi - ylo - 1));
+      g.set(xhi, y, CELL_EMPTY);
+      xlo = xhi;
+      xhi = next_limit(vmask, xlo, W - 1);
+    } else {                        // 'v': through the horizontal river at y = yhi
+      const int x = xlo + 1 + (int)ds.next_bounded((uint32_t)(xhi - xlo - 1));
+      g.set(x, yhi, CELL_EMPTY);
+      ylo = yhi;
+      yhi = next_limit(hmask, ylo, H - 1);
+    }
+  }
+}
+
 // WARP: the whole warp calls this for ONE env (same arguments in every lane,
 // converged) and KeyCorridor's connect_all runs 32 of its iterations at once
 // (see the loop); every other family and step is computed redundantly.
@@ -381,69 +457,17 @@ __device__ __noinline__ GenOut generate_level(RowViewT<Cfg<FAM, H, W>::RW> g, ui
     const int ty = t == 0 ? 0 : t == 1 ? h - 1 : t == 2 ? d2 : d3;
     o.target = (uint32_t)((tx << 4) | ty);
   } else if constexpr (FAM == FAM_CROSSING) {
-    // [MG] CrossingEnv._gen_grid, obstacle Wall or Lava (gparam & CROSSING_LAVA),
-    // N = gparam & 0xff crossings; the two
-    // shuffles as R#35 reads them.  Rivers are nibbles (bit 3: horizontal,
-    // bits 0-2: position / 2 - 1): (S-3)/2 vertical ones, then as many horizontal.
-    constexpr int NRV = (W - 3) / 2, M = 2 * NRV;
+    // the Table 8 / 9 crossing counts get a generator with N known at compile
+    // time: its 3N - 1 draws come from Philox blocks computed up front
+    // (independent chains), each at a compile-time word
     const int N = gparam & 0xff;
     const uint8_t obstacle = (gparam & CROSSING_LAVA) ? CELL_LAVA : CELL_WALL;
-    uint64_t riv = 0;
-#pragma unroll
-    for (int k = 0; k < M; ++k) riv |= (uint64_t)((k < NRV ? 0 : 8) | (k % NRV)) << (4 * k);
-    uint32_t vmask = 0, hmask = 0;  // bit p: a vertical river at x = p / a horizontal one at y = p
-    for (int k = 0; k < N; ++k) {
-      const int j = k + (int)ds.next_bounded((uint32_t)(M - k));
-      const uint64_t a = (riv >> (4 * k)) & 15, b = (riv >> (4 * j)) & 15;
-      riv = (riv & ~(15ull << (4 * k)) & ~(15ull << (4 * j))) | (b << (4 * k)) | (a << (4 * j));
-      const uint32_t bit = 1u << (2 * ((b & 7) + 1));
-      if (b & 8) hmask |= bit; else vmask |= bit;
-    }
-    // the rivers, a whole row plane at a time: plane q of an interior row is
-    // obstacle at the interior bytes if the row is a horizontal river, else at
-    // the vertical rivers' bytes (a byte mask spread from vmask's bits)
-    {
-      const uint64_t obst8 = 0x0101010101010101ull * obstacle;
-      uint64_t vm[C::RW];
-#pragma unroll
-      for (int q = 0; q < C::RW; ++q) vm[q] = bits_to_bytes((vmask >> (8 * q)) & 0xFFu);
-#pragma unroll
-      for (int y = 1; y < H - 1; ++y) {
-        const bool hr = (hmask >> y) & 1u;
-#pragma unroll
-        for (int q = 0; q < C::RW; ++q) {
-          const uint64_t m = hr ? interior_bytes<W>(q) : vm[q];
-          g.rows[(y * C::RW + q) * TILE] = (template_plane<FAM, H, W>(y * C::RW + q) & ~m) | (obst8 & m);
-        }
-      }
-    }
-    // path: popc(vmask) 'h' moves then popc(hmask) 'v' moves (bit k = 1: 'v'), Fisher-Yates
-    const int nv = __popc(vmask);
-    uint32_t path = ((1u << N) - 1) & ~((1u << nv) - 1);
-    for (int i = N - 1; i >= 1; --i) {
-      const int j = (int)ds.next_bounded((uint32_t)(i + 1));
-      const uint32_t bi = (path >> i) & 1u, bj = (path >> j) & 1u;
-      path = (path & ~(1u << i) & ~(1u << j)) | (bj << i) | (bi << j);
-    }
-    // openings: the current room spans x in (xlo, xhi), y in (ylo, yhi)
-    auto next_limit = [](uint32_t m, int lo, int end) {
-      const uint32_t above = m & ~((2u << lo) - 1);
-      return above ? __ffs(above) - 1 : end;
-    };
-    int xlo = 0, ylo = 0;
-    int xhi = next_limit(vmask, 0, W - 1), yhi = next_limit(hmask, 0, H - 1);
-    for (int k = 0; k < N; ++k) {
-      if (((path >> k) & 1u) == 0) {  // 'h': through the vertical river at x = xhi
-        const int y = ylo + 1 + (int)ds.next_bounded((uint32_t)(yhi - ylo - 1));
-        g.set(xhi, y, CELL_EMPTY);
-        xlo = xhi;
-        xhi = next_limit(vmask, xlo, W - 1);
-      } else {                        // 'v': through the horizontal river at y = yhi
-        const int x = xlo + 1 + (int)ds.next_bounded((uint32_t)(xhi - xlo - 1));
-        g.set(x, yhi, CELL_EMPTY);
-        ylo = yhi;
-        yhi = next_limit(hmask, ylo, H - 1);
-      }
+    switch (N) {
+      case 1: { FixedDraws<1> fd(genv, episode, klo, khi); crossing_level<H, W, 1>(g, fd, 1, obstacle); break; }
+      case 2: { FixedDraws<2> fd(genv, episode, klo, khi); crossing_level<H, W, 2>(g, fd, 2, obstacle); break; }
+      case 3: { FixedDraws<2> fd(genv, episode, klo, khi); crossing_level<H, W, 3>(g, fd, 3, obstacle); break; }
+      case 5: { FixedDraws<4> fd(genv, episode, klo, khi); crossing_level<H, W, 5>(g, fd, 5, obstacle); break; }
+      default: crossing_level<H, W, 0>(g, ds, N, obstacle); break;
     }
   } else if constexpr (FAM == FAM_DOORKEY) {
     // [MG] DoorKeyEnv._gen_grid: split, agent pos, agent dir, door row, key pos
