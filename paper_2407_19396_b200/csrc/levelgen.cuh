@@ -249,7 +249,8 @@ struct FixedDraws {
 
 // The draw source of generate_level: one thread's DrawStream, the warp's
 // cache (KeyCorridor generated by a whole warp), or the prefetched blocks of
-// a fixed draw sequence (GoToDoor 13 draws, DoorKey 5, FourRooms 7).
+// a fixed draw sequence (GoToDoor 13 draws, DoorKey 5, FourRooms 7, LavaGap
+// and Empty-Random 2; the Crossings pick theirs per crossing count).
 template <int FAM, bool WARP>
 struct LevelDrawsT {
   using type = DrawStream;
@@ -269,6 +270,14 @@ struct LevelDrawsT<FAM_DOORKEY, WARP> {
 template <bool WARP>
 struct LevelDrawsT<FAM_FOURROOMS, WARP> {
   using type = FixedDraws<2>;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_LAVAGAP, WARP> {  // the gap column and row
+  using type = FixedDraws<1>;
+};
+template <bool WARP>
+struct LevelDrawsT<FAM_EMPTY_RANDOM, WARP> {  // the agent's cell and direction
+  using type = FixedDraws<1>;
 };
 __device__ __forceinline__ DrawStream make_draws(DrawStream*, uint32_t env, uint32_t ep, uint32_t klo, uint32_t khi) {
   return DrawStream(env, ep, 0u, klo, khi);
