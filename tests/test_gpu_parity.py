@@ -88,6 +88,13 @@ def test_parity_cfg5_doorkey_1M_sampled():
     run_parity("DoorKey-8x8-v0", 1 << 20, 300, block=96, export_every=100)
 
 
+@pytest.mark.parametrize("env_id", ["DoorKey-8x8-v0", "Dynamic-Obstacles-8x8-v0"])
+def test_parity_max_size_ragged_sampled(env_id):
+    # [CFG 5]'s largest size, 2^23 envs per GPU, plus a ragged tail of 77:
+    # head, middle and tail blocks against the oracle, the state at the end
+    run_parity(env_id, (1 << 23) + 77, 40, block=96, export_every=1000)
+
+
 @pytest.mark.parametrize("env_id", ["Empty-6x6-v0", "DoorKey-5x5-v0", "DoorKey-6x6-v0",
                                     "Dynamic-Obstacles-5x5-v0", "Dynamic-Obstacles-6x6-v0",
                                     "LavaGapS5-v0", "LavaGapS6-v0", "KeyCorridorS3R1-v0",
