@@ -154,9 +154,10 @@ def main():
     configs = [(e, 1 << 20) for e in CATALOG] if a.catalog else CONFIGS
     if a.catalog and not a.sizes:
         sizes = CATALOG_SIZES
+    if envs:  # the ids asked for, in the order given (ids outside CONFIGS up to 2^20 envs)
+        known = dict(configs)
+        configs = [(e, known.get(e, 1 << 20)) for e in a.envs.split(",") if e]
     for env_id, nmax in configs:
-        if envs and env_id not in envs:
-            continue
         for n in sizes:
             if n > nmax:
                 continue
