@@ -196,7 +196,7 @@ NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_e
  * runs the multi-lane-per-env kernels (8 lanes share an env and split its
  * observation by view column), larger ones the one-thread-per-env kernels.
  * Results are bit-identical either way; only the latency differs.  Defaults:
- * 1024 envs for steps (NAVIX_DEFAULT_WIDE_MAX, environment variable
+ * 2048 envs for steps (NAVIX_DEFAULT_WIDE_MAX, environment variable
  * NAVIX_WIDE_MAX) and 4096 for rollouts (NAVIX_DEFAULT_WIDE_MAX_ROLLOUT,
  * NAVIX_WIDE_MAX_ROLLOUT); this call sets both; 0 disables.  Grids up to 8
  * wide except GoToDoor.  Host only; graphs captured earlier keep the old

@@ -36,7 +36,7 @@ namespace navix {
 
 constexpr int TILE = 128;   // envs per CTA (one thread per env)
 #ifndef NAVIX_DEFAULT_WIDE_MAX
-#define NAVIX_DEFAULT_WIDE_MAX 1024  // small-batch kernel up to this many envs (measured)
+#define NAVIX_DEFAULT_WIDE_MAX 2048  // small-batch kernel up to this many envs (measured)
 #endif
 #ifndef NAVIX_DEFAULT_WIDE_MAX_ROLLOUT
 #define NAVIX_DEFAULT_WIDE_MAX_ROLLOUT 4096  // the same for rollouts (measured)

@@ -1601,8 +1601,11 @@ inline int64_t env_switch_persist_ctas() {
   static const int64_t v = [] { const char* e = getenv("NAVIX_PERSIST_CTAS"); return e ? (int64_t)atoll(e) : (int64_t)0; }();
   return v;
 }
-inline int env_switch_pdl() {
-  static const int v = [] { const char* e = getenv("NAVIX_PDL"); return e && e[0] == '0' ? 0 : 1; }();
+inline int env_switch_pdl() {  // NAVIX_PDL=0: no PDL anywhere; =2: also on the small-batch step (A/B)
+  static const int v = [] {
+    const char* e = getenv("NAVIX_PDL");
+    return e && e[0] == '0' ? 0 : e && e[0] == '2' ? 2 : 1;
+  }();
   return v;
 }
 
@@ -1672,15 +1675,22 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   constexpr bool WIDE_OK = C::RW == 1 && FAM != FAM_GOTODOOR;
   if constexpr (WIDE_OK) {
     if (mode == MODE_STEP && a.n <= a.wide_max) {
+      // programmatic dependent launch only for grids of <= 48 CTAs (768
+      // envs): there it hides the launch (2-8 %); on larger grids the next
+      // step's CTAs, launched at once, sit on the SMs beside the running ones
+      // and back-to-back steps ran 20-85 % slower from 1,536 envs on
+      // (DESIGN.md §6.5); NAVIX_PDL=2 turns it on at every size (A/B)
+      const unsigned wgrid = (unsigned)((a.n + WIDE_EPC - 1) / WIDE_EPC);
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)((a.n + WIDE_EPC - 1) / WIDE_EPC));
+      cfg.gridDim = dim3(wgrid);
       cfg.blockDim = block;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      const int pdl = env_switch_pdl();
+      cfg.numAttrs = pdl == 2 || (pdl == 1 && wgrid <= 48u) ? 1 : 0;
       return cudaLaunchKernelEx(&cfg, navix_step_wide<FAM, H, W, OBSK>, a);
     }
   }
