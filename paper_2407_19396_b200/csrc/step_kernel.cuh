@@ -1713,7 +1713,13 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       if (env_switch_persist_ctas() > 0) cap = env_switch_persist_ctas();
       const unsigned grid = (unsigned)(n_tiles < cap ? n_tiles : cap);
       // launched with programmatic stream serialization (PDL): back-to-back
-      // steps overlap the launch of step t+1 with the tail of step t
+      // steps overlap the launch of step t+1 with the tail of step t.  That
+      // pays when the grid is full and the tiles fill its waves; when slots
+      // stay free (fewer tiles than CTA slots, or a second wave less than
+      // nine-tenths empty) the next step's CTAs launched into them slowed
+      // the running ones: 8,192 - 131,072 envs 5-29 % faster without it,
+      // 98,304 and >= 196,608 envs 1-5 % slower
+      const bool pdl_pays = n_tiles >= cap && (n_tiles >= 2 * cap || 10 * (n_tiles - cap) < cap);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = block;
@@ -1723,7 +1729,8 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
-      cfg.numAttrs = env_switch_pdl() ? 1 : 0;
+      const int pdl = env_switch_pdl();
+      cfg.numAttrs = pdl == 2 || (pdl == 1 && pdl_pays) ? 1 : 0;
       return cudaLaunchKernelEx(&cfg, navix_step_persistent<FAM, H, W, OBSK>, a);
     }
   } else if (mode == MODE_OBS_TABLE) {
