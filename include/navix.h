@@ -199,7 +199,7 @@ NAVIX_API navix_status navix_set_event_functions(navix_env* h, uint32_t reward_e
  * 2048 envs for steps (NAVIX_DEFAULT_WIDE_MAX, environment variable
  * NAVIX_WIDE_MAX) and 4096 for rollouts (NAVIX_DEFAULT_WIDE_MAX_ROLLOUT,
  * NAVIX_WIDE_MAX_ROLLOUT); this call sets both; 0 disables.  Grids up to 8
- * wide except GoToDoor.  Host only; graphs captured earlier keep the old
+ * wide except GoToDoor (and KeyCorridor steps).  Host only; graphs captured earlier keep the old
  * choice. */
 NAVIX_API navix_status navix_set_small_batch_threshold(navix_env* h, int64_t max_envs);
 

@@ -1674,7 +1674,11 @@ cudaError_t launch_fhwk(int mode, const KernelArgs& a, int64_t n_tiles, cudaStre
   // small batches: the multi-lane-per-env kernel (navix_step_wide)
   constexpr bool WIDE_OK = C::RW == 1 && FAM != FAM_GOTODOOR;
   if constexpr (WIDE_OK) {
-    if (mode == MODE_STEP && a.n <= a.wide_max) {
+    // KeyCorridor steps never take it: its level generator runs per lane
+    // there (no warp-cooperative connect_all), and with steady-state resets
+    // (episodes desynchronised) that lost at every size measured (512 envs
+    // 13.2 us per step vs ~9.5 on the persistent kernel, 2,048: 19.1 vs 10.3)
+    if (mode == MODE_STEP && FAM != FAM_KEYCORRIDOR && a.n <= a.wide_max) {
       // programmatic dependent launch only for grids of <= 48 CTAs (768
       // envs): there it hides the launch (2-8 %); on larger grids the next
       // step's CTAs, launched at once, sit on the SMs beside the running ones
